@@ -1,0 +1,363 @@
+"""Benchmark of the tiled D3Q19 LBGK step on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N = 1 workload: BASELINE config 2 -- dense square channel 256^3, bounce-back
+ring, periodic along x, LBGK incompressible, fp64, tau = 0.6, started from a
+perturbed equilibrium (paper_1611_02445_b200/workloads.py).  One "step" = one
+launch of the fused collide+propagate kernel over all 262,144 tiles.  The
+field (2 x 2.55 GB) is far larger than L2 (126 MB), so no flush is needed.
+
+N > 1 (torchrun, one rank per GPU): weak scaling -- every rank owns a
+256^3 z-slab of a 256 x 256 x 256N periodic-x channel; ghost tile layers are
+exchanged every step over NCCL (paper_1611_02445_b200/slabs.py).
+
+Reported (one JSON line on rank 0):
+  value      MLUPS over all ranks (non-solid node updates / s / 1e6), device
+             time from CUDA events on the launching stream, max over ranks
+  roofline   algorithmic bytes per launch = n_fn x 2 x 19 x 8 B (txmodel
+             b_node) / average launch time, vs MEASURED_PEAKS.json hbm_gbs;
+             traffic = ncu dram bytes per launch (profiles/roofline_traffic.json)
+  e2e        the same metric through the public API from host data: geometry
+             upload, device tiling, init, K steps each followed by an async
+             D2H of the step's status word, final rho/u readout to the host
+  cpu_baseline  the C oracle (oracle/tlbm_oracle.c, OpenMP on all host cores)
+             on a bounded sample of the same workload (rank 0, N = 1)
+  --impl reference  times that same CPU oracle as the reference arm
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "D3Q19 fp64 MFLUPS and % of peak HBM GB/s vs porosity at 1/2/4/8 B200"
+UNIT = "MFLUPS"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    p.add_argument("--n", type=int, default=256, help="channel edge (nodes)")
+    p.add_argument("--table", default="b200")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, index, period=0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as exc:  # pragma: no cover - depends on the box
+            self.err = str(exc)
+
+    def _run(self):
+        n = self.nvml
+        names = {
+            "hw_slowdown": getattr(n, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(n, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(n, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(n, "nvmlClocksEventReasonHwPowerBrakeSlowdown",
+                                               0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM))
+                r = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def report(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [],
+                    "note": getattr(self, "err", "no samples")}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def traffic_from_profiles(key):
+    path = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if not os.path.exists(path):
+        return None
+    d = json.load(open(path))
+    return d.get(key)
+
+
+# ---------------------------------------------------------------- CPU oracle
+def cpu_oracle_mlups(precision, n, seconds, threads=0):
+    """C oracle (OpenMP, `threads` = all available) on a bounded sample of the
+    channel workload: the same 256 x 256 cross-section, 32 nodes along the
+    periodic axis (per-node work is identical along the channel)."""
+    from oracle import c_oracle, dense
+    from paper_1611_02445_b200 import workloads
+    dt = np.float64 if precision == "f64" else np.float32
+    length = 32
+    geo = workloads.channel(n, length=length)
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.05, 0.0, 0.0))
+    cores = threads or len(os.sched_getaffinity(0))
+    o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
+                             f0=f0, dtype=dt, nthreads=cores)
+    n_fn = geo.nonsolid_count()
+    o.run(1)                                     # warm-up (page faults, threads)
+    steps, t0 = 0, time.perf_counter()
+    while True:
+        o.run(1)
+        steps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or steps >= 200:
+            break
+    return {"value": n_fn * steps / el / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"C oracle (oracle/tlbm_oracle.c, OpenMP x{cores}) on the channel "
+                      f"{length}x{n}x{n} slab (periodic x), {precision}, {steps} steps "
+                      f"in {el:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    t_all = []
+    from oracle import c_oracle, dense
+    from paper_1611_02445_b200 import workloads
+    dt = np.float64 if args.precision == "f64" else np.float32
+    length = 32
+    geo = workloads.channel(args.n, length=length)
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.05, 0.0, 0.0))
+    cores = len(os.sched_getaffinity(0))
+    o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
+                             f0=f0, dtype=dt, nthreads=cores)
+    n_fn = geo.nonsolid_count()
+    for _ in range(args.warmup):
+        o.run(1)
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        o.run(1)
+        t_all.append(time.perf_counter() - t0)
+    total = sum(t_all)
+    value = n_fn * args.steps / total / 1e6
+    sample = (f"C oracle port (oracle/tlbm_oracle.c, OpenMP x{cores}): each step = one full "
+              f"step of the channel {length}x{args.n}x{args.n} slab (periodic x), "
+              f"{args.precision}; the reference has no step of its own (SURVEY 0.2)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": f"channel{args.n}_periodic_{args.precision}",
+                       "sample_nodes": n_fn},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def timed_steps(solver, steps, torch):
+    """K steps bracketed by synchronize + CUDA events on the launching
+    stream; returns elapsed ms."""
+    stream = torch.cuda.current_stream()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    solver.step(steps, check=False)
+    end.record(stream)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end)
+
+
+def e2e_run(args, torch, geo_host):
+    """Public API end to end from host data: Solver(geometry) [H2D of the
+    tags, device tiler + metadata, init], K x step() each with an async D2H of
+    that step's status word to pinned memory, final macroscopic readout."""
+    from paper_1611_02445_b200 import solver as sv
+    cfg = sv.SimulationConfig(tau=0.6, precision=args.precision, table=args.table)
+    pinned = torch.empty(args.steps, dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = sv.Solver(geo_host, cfg)
+    s.init_equilibrium(1.0, (0.05, 0.0, 0.0))
+    for i in range(args.steps):
+        s.step(1, check=False)
+        slot = (s.iteration - 1) % sv.STATUS_RING
+        pinned[i:i + 1].copy_(s.status[slot:slot + 1], non_blocking=True)
+    rho, u, _ = s.macroscopic(device=False)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if np.any(pinned.numpy() & 1):
+        raise RuntimeError("e2e run diverged")
+    h2d = geo_host.types.nbytes
+    d2h = 4 * args.steps + rho.nbytes + u.nbytes
+    n_fn = s.n_fn
+    del s
+    return {"value": n_fn * args.steps / el / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "seconds": el,
+            "what": "Solver(geometry) + init + K x step() with per-step async D2H of the "
+                    "status word + final rho/u readout, host numpy in/out"}
+
+
+def run_b200(args):
+    import torch
+    from paper_1611_02445_b200 import _native as nat
+    from paper_1611_02445_b200 import txmodel, workloads
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_1611_02445_b200 import slabs
+        runner = slabs.SlabChannel(args.n, world, rank, precision=args.precision,
+                                   table=args.table)
+        n_fn_rank = runner.n_fn_owned
+        step_fn = runner.step
+        sync_all = runner.barrier
+    else:
+        geo = workloads.channel(args.n)
+        solver = workloads.make_solver(geo, precision=args.precision, table=args.table)
+        n_fn_rank = solver.n_fn
+        step_fn = lambda k: solver.step(k, check=False)  # noqa: E731
+        sync_all = lambda: None  # noqa: E731
+        runner = solver
+
+    for _ in range(args.warmup):
+        step_fn(1)
+    torch.cuda.synchronize()
+    sync_all()
+
+    stream = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        sync_all()
+        start.record(stream)
+        step_fn(args.steps)
+        end.record(stream)
+        torch.cuda.synchronize()
+        sync_all()
+    ms = start.elapsed_time(end)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        nf = torch.tensor([n_fn_rank], device="cuda", dtype=torch.float64)
+        dist.all_reduce(nf)
+        n_fn_total = int(nf.item())
+    else:
+        n_fn_total = n_fn_rank
+    # divergence check outside the timed region
+    if world == 1:
+        solver.check()
+
+    ms_step = ms / args.steps
+    value = n_fn_total * args.steps / (ms / 1e3) / 1e6
+    n_d = 8 if args.precision == "f64" else 4
+    b_node = txmodel.b_node(19, n_d)
+    alg_bytes = n_fn_rank * b_node
+    achieved = alg_bytes / (ms_step / 1e3) / 1e9
+    peak, peak_src = peaks()
+    key = f"channel{args.n}_{args.precision}_{args.table}"
+    traffic = traffic_from_profiles(key)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": f"channel{args.n}_periodic_{args.precision}"
+                               + (f"_slab_x{world}" if world > 1 else ""),
+                   "geometry": f"square channel d={args.n}, BB ring, periodic x, "
+                               f"{args.n}x{args.n}x{args.n} per GPU",
+                   "model": "LBGK incompressible, tau=0.6", "layout_table": args.table,
+                   "n_fn_per_gpu": n_fn_rank, "t_n_per_gpu": n_fn_rank // 64,
+                   "l2": "inputs larger than L2 (field %.2f GB per copy)"
+                         % (n_fn_rank / 64 * 19 * 64 * n_d / 1e9),
+                   "parallelism": f"slab{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_node": b_node,
+                     "metadata_bytes_per_launch": txmodel.metadata_bytes(n_fn_rank // 64),
+                     "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
+        "clocks": clocks.report(),
+        "gpu_launches": args.steps,
+    }
+    if rank == 0 and world == 1 and not args.no_e2e:
+        del runner, solver
+        torch.cuda.empty_cache()
+        line["e2e"] = e2e_run(args, torch, workloads.channel(args.n))
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_oracle_mlups(args.precision, args.n, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

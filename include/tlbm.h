@@ -1,0 +1,147 @@
+/*
+ * tlbm.h -- C ABI of the B200 tiled sparse-geometry D3Q19 LBM path
+ * (libtlbm.so, built from paper_1611_02445_b200/csrc/ for sm_100a).
+ *
+ * The reference (`tilelbm`, /root/reference/pkg/src/tilelbm) is pure Python
+ * with no FFI; each entry point below replaces the reference function named
+ * beside it, and the Python host mirror (paper_1611_02445_b200/*.py) keeps the
+ * reference's names and shapes on top of these calls via ctypes.
+ *
+ * Conventions
+ *   - Every pointer prefixed d_ is device memory owned by the caller
+ *     (allocated by PyTorch); the library never allocates persistent memory
+ *     and never frees caller memory.  Pointers prefixed h_ are host memory.
+ *   - `stream` is a cudaStream_t; every call is asynchronous on it unless its
+ *     comment says it synchronises.
+ *   - Return value: 0 on success, otherwise a TLBM_ERR_* code; the message
+ *     is in tlbm_last_error() (thread-local).
+ *   - dtype: TLBM_F64 / TLBM_F32.  fluid: TLBM_INCOMPRESSIBLE / TLBM_QUASI
+ *     (collision.py:28-30).  table: TLBM_TABLE_* (layout.py:34-36 + B200).
+ *   - Field store: one copy is t_n * 19 * 64 values, block (tile, q) at
+ *     ((tile * 19) + q) * 64, slot inside the block given by the table's
+ *     layout for q (layout.py:115-132 with copy-major order for two copies).
+ */
+#ifndef TLBM_H
+#define TLBM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TLBM_ABI_VERSION 1
+
+enum { TLBM_F64 = 0, TLBM_F32 = 1 };
+enum { TLBM_INCOMPRESSIBLE = 0, TLBM_QUASI = 1 };
+enum { TLBM_TABLE_XYZ = 0, TLBM_TABLE_OPTIMIZED = 1, TLBM_TABLE_B200 = 2 };
+enum { TLBM_OK = 0, TLBM_ERR_ARG = 1, TLBM_ERR_CUDA = 2 };
+/* step variants (SPEC.md:531-539 bench ladder) */
+enum { TLBM_FULL = 0, TLBM_PROPAGATION_ONLY = 1, TLBM_READ_WRITE_ONLY = 2 };
+/* bits of the device status word written by tlbm_step / tlbm_macroscopic */
+enum { TLBM_FLAG_DIVERGED = 1, TLBM_FLAG_GUARD = 2 };
+
+int tlbm_abi_version(void);
+const char *tlbm_last_error(void);
+int tlbm_set_device(int device);
+
+/* Host-only: the compiled-in lattice and layout tables, for CPU checks.
+ * e: 19x3 int32, opp: 19 int32, w: 19 double, perm: 19x64 int32 slot
+ * permutation of `table` (layout.py:108-112 table_permutations). */
+int tlbm_lattice_tables(int table, int32_t *h_e, int32_t *h_opp, double *h_w,
+                        int32_t *h_perm);
+
+/* ---- tiler (replaces tiling.py:51-83 build_tiling) ---------------------- */
+/* Scratch bytes needed by tlbm_tile_map for an nx*ny*nz grid. */
+size_t tlbm_tiling_scratch_bytes(int nx, int ny, int nz);
+/* Occupancy of every 4^3 tile of the SOLID-padded grid and the order-stable
+ * compaction in (z outer, y, x inner) scan order.  Writes d_tile_map
+ * (ntx, nty, ntz) C-order int32 (-1 = empty) and *h_t_n.  Synchronises
+ * `stream` (t_n is needed to size every other buffer). */
+int tlbm_tile_map(const uint8_t *d_types, int nx, int ny, int nz,
+                  int32_t *d_tile_map, void *d_scratch, int64_t *h_t_n,
+                  void *stream);
+/* Corner coordinates of the non-empty tiles, (t_n, 3) int32. */
+int tlbm_tile_list(const int32_t *d_tile_map, int ntx, int nty, int ntz,
+                   int32_t *d_non_empty, int64_t t_n, void *stream);
+/* Neighbour tile index for all 27 deltas (dx,dy,dz) in itertools.product
+ * order, (t_n, 27) int32, -1 absent/outside; periodic_mask bit a wraps axis a
+ * (replaces txmodel.py:145-160 _neighbor_indices). */
+int tlbm_tile_neighbors(const int32_t *d_tile_map, int ntx, int nty, int ntz,
+                        const int32_t *d_non_empty, int64_t t_n,
+                        int periodic_mask, int32_t *d_nbr, void *stream);
+/* Per-slot node metadata word (see csrc/d3q19.cuh), (t_n, 64) uint32; also
+ * counts into *d_bad the inlet/outlet nodes not on exactly one domain face
+ * (boundaries.py:95-129 classify_boundary_faces rejects those). */
+int tlbm_node_meta(const uint8_t *d_types, int nx, int ny, int nz,
+                   int periodic_mask, const int32_t *d_non_empty, int64_t t_n,
+                   uint32_t *d_meta, int32_t *d_bad, void *stream);
+/* Non-solid node count per tile, (t_n,) int32 (tiling.py:141-152). */
+int tlbm_tile_counts(const uint32_t *d_meta, int64_t t_n, int32_t *d_counts,
+                     void *stream);
+
+/* ---- field store (replaces layout.py:135-167 FieldStore I/O) ------------ */
+/* One copy := equilibrium(rho, u) in all 64 slots of every tile
+ * (collision.py:94-121). */
+int tlbm_init_equilibrium(void *d_f, int dtype, int fluid, int table,
+                          int64_t t_n, double rho, double ux, double uy,
+                          double uz, void *stream);
+/* One copy := equilibrium(rho[t,j], u[:,t,j]) from canonical (t_n,64) rho and
+ * (3,t_n,64) u of the working dtype. */
+int tlbm_init_from_macroscopic(void *d_f, int dtype, int fluid, int table,
+                               int64_t t_n, const void *d_rho, const void *d_u,
+                               void *stream);
+/* Stored blocks <-> canonical (19, t_n, 64) (layout.py:155-167). */
+int tlbm_to_canonical(const void *d_f, int dtype, int table, int64_t t_n,
+                      void *d_canon, void *stream);
+int tlbm_from_canonical(const void *d_canon, int dtype, int table,
+                        int64_t t_n, void *d_f, void *stream);
+/* rho (t_n,64), u (3,t_n,64), p (t_n,64) of one copy in canonical order
+ * (collision.py:75-91 applied to read_canonical); d_p may be NULL.  Sets
+ * TLBM_FLAG_DIVERGED in *d_flags for rho <= 0 (quasi) or NaN. */
+int tlbm_macroscopic(const void *d_f, int dtype, int fluid, int table,
+                     int64_t t_n, void *d_rho, void *d_u, void *d_p,
+                     uint32_t *d_flags, void *stream);
+/* Dense-array macroscopic of canonical f (19, n): rho (n), u (3, n), p (n)
+ * (collision.py:75-91 on arbitrary node batches). */
+int tlbm_macroscopic_canonical(const void *d_f, int dtype, int fluid,
+                               int64_t n, void *d_rho, void *d_u, void *d_p,
+                               uint32_t *d_flags, void *stream);
+/* equilibrium (19, n) from rho (n), u (3, n) (collision.py:94-121). */
+int tlbm_equilibrium(const void *d_rho, const void *d_u, int dtype, int fluid,
+                     int64_t n, void *d_feq, void *stream);
+/* collide_lbgk on (19, n) canonical populations in place (collision.py:124). */
+int tlbm_collide_lbgk(void *d_f, int dtype, int fluid, int64_t n, double tau,
+                      uint32_t *d_flags, void *stream);
+/* Zou-He closure in place on (19, m) canonical populations of nodes on one
+ * face (face = 2*axis + (0 low | 1 high)); kind 0 = velocity inlet with
+ * (ux,uy,uz) (boundaries.py:139-157), 1 = pressure outlet with rho0
+ * (boundaries.py:160-176).  d_ret (m), optional, receives the implied density
+ * (kind 0) or normal momentum (kind 1) the reference returns. */
+int tlbm_zou_he(void *d_g, int dtype, int fluid, int face, int kind, int64_t m,
+                double ux, double uy, double uz, double rho0, void *d_ret,
+                void *stream);
+
+/* ---- the step (Alg. 2; boundaries.py:1-28) ------------- */
+typedef struct {
+    int dtype, fluid, table, variant;
+    int64_t t_n;                 /* tiles in the store */
+    int64_t tile_begin, tile_end;/* range of tiles updated by this launch */
+    const void *f_src;           /* current copy */
+    void *f_dst;                 /* other copy */
+    const int32_t *nbr;          /* (t_n, 27) */
+    const uint32_t *meta;        /* (t_n, 64) */
+    double tau;
+    double inlet_u[3];
+    double outlet_rho;
+    double u_guard;              /* |u| > u_guard sets TLBM_FLAG_GUARD; 0 off */
+    uint32_t *flags;             /* device status word (OR-ed), may be NULL */
+} tlbm_step_args;
+
+int tlbm_step(const tlbm_step_args *a, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TLBM_H */

@@ -1,0 +1,287 @@
+// Field-store kernels: equilibrium initialisation, canonical
+// scatter/gather (layout.py:155-167) and the macroscopic readout
+// (collision.py:75-121) -- all in the reference's arithmetic order.
+#include "common.cuh"
+#include "physics.cuh"
+
+namespace tlbm {
+namespace {
+
+constexpr int TILE_VALUES = Q * 64;
+
+__device__ __forceinline__ long long gtid() {
+    return blockIdx.x * (long long)blockDim.x + threadIdx.x;
+}
+__device__ __forceinline__ long long gstride() { return (long long)gridDim.x * blockDim.x; }
+
+unsigned grid_capped(long long n) {
+    long long g = (n + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return (unsigned)g;
+}
+
+template <class T, int QUASI, int TABLE>
+__global__ void init_uniform_kernel(T *f, long long t_n, double rho_d, double ux, double uy,
+                                    double uz) {
+    for (long long i = gtid(); i < t_n * 64; i += gstride()) {
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+        const T rho = T(rho_d);
+        const T u[3] = {T(ux), T(uy), T(uz)};
+        const T usq = speed_sq(u);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            f[t * TILE_VALUES + q * 64 + slot_of<TABLE>(q, j & 3, (j >> 2) & 3, j >> 4)] =
+                equilibrium_q<T, QUASI>(q, rho, u, usq);
+    }
+}
+
+template <class T, int QUASI, int TABLE>
+__global__ void init_fields_kernel(T *f, long long t_n, const T *rho, const T *u) {
+    const long long n = t_n * 64;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+        const T r = rho[i];
+        const T uu[3] = {u[i], u[n + i], u[2 * n + i]};
+        const T usq = speed_sq(uu);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            f[t * TILE_VALUES + q * 64 + slot_of<TABLE>(q, j & 3, (j >> 2) & 3, j >> 4)] =
+                equilibrium_q<T, QUASI>(q, r, uu, usq);
+    }
+}
+
+template <class T, int TABLE, bool TO_CANON>
+__global__ void canon_kernel(const T *in, T *out, long long t_n) {
+    const long long n = t_n * 64;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const long long blk = t * TILE_VALUES + q * 64 + slot_of<TABLE>(q, j & 3, (j >> 2) & 3, j >> 4);
+            const long long can = q * n + i;
+            if (TO_CANON) out[can] = in[blk];
+            else out[blk] = in[can];
+        }
+    }
+}
+
+template <class T, int QUASI>
+__device__ __forceinline__ uint32_t readout(const T (&g)[Q], long long i, long long n, T *rho,
+                                            T *u, T *p) {
+    T r, uu[3];
+    moments<T, QUASI>(g, r, uu);
+    rho[i] = r;
+    u[i] = uu[0];
+    u[n + i] = uu[1];
+    u[2 * n + i] = uu[2];
+    if (p) p[i] = r / T(3.0);
+    return status_of<T, QUASI>(r, T(0), 0.0);
+}
+
+template <class T, int QUASI, int TABLE>
+__global__ void macro_blocks_kernel(const T *f, long long t_n, T *rho, T *u, T *p,
+                                    uint32_t *flags) {
+    const long long n = t_n * 64;
+    uint32_t st = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+            g[q] = f[t * TILE_VALUES + q * 64 + slot_of<TABLE>(q, j & 3, (j >> 2) & 3, j >> 4)];
+        st |= readout<T, QUASI>(g, i, n, rho, u, p);
+    }
+    if (flags && st) atomicOr(flags, st);
+}
+
+template <class T, int QUASI>
+__global__ void macro_canon_kernel(const T *f, long long n, T *rho, T *u, T *p,
+                                   uint32_t *flags) {
+    uint32_t st = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g[q] = f[q * n + i];
+        st |= readout<T, QUASI>(g, i, n, rho, u, p);
+    }
+    if (flags && st) atomicOr(flags, st);
+}
+
+template <class T, int QUASI>
+__global__ void equilibrium_kernel(const T *rho, const T *u, long long n, T *feq) {
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const T uu[3] = {u[i], u[n + i], u[2 * n + i]};
+        const T usq = speed_sq(uu);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) feq[q * n + i] = equilibrium_q<T, QUASI>(q, rho[i], uu, usq);
+    }
+}
+
+template <class T, int QUASI>
+__global__ void collide_kernel(T *f, long long n, double inv_tau, uint32_t *flags) {
+    uint32_t st = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g[q] = f[q * n + i];
+        st |= collide<T, QUASI>(g, T(inv_tau), 0.0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) f[q * n + i] = g[q];
+    }
+    if (flags && st) atomicOr(flags, st);
+}
+
+template <class T, int QUASI, int FACE>
+__device__ __forceinline__ T zou_he_node(T (&g)[Q], int kind, const double (&u_in)[3],
+                                         double rho0) {
+    // value returned by zou_he_velocity (implied rho) / zou_he_pressure (jn);
+    // k0 and km are untouched by the closure (c.n <= 0)
+    const T k0 = ordered_sum<T, FACE>(g, 0, -1, 0);
+    const T km = ordered_sum<T, FACE>(g, -1, -1, 0);
+    T ret;
+    if (kind == 0) {
+        const T un = T(face_sign(FACE)) * T(u_in[face_axis(FACE)]);
+        ret = QUASI ? (k0 + T(2.0) * km) / (T(1.0) - un) : k0 + T(2.0) * km + un;
+        zh_velocity<T, QUASI, FACE>(g, u_in);
+    } else {
+        ret = T(rho0) - (k0 + T(2.0) * km);
+        zh_pressure<T, FACE>(g, rho0);
+    }
+    return ret;
+}
+
+template <class T, int QUASI, int FACE>
+__global__ void zou_he_kernel(T *g_all, long long m, int kind, double ux, double uy, double uz,
+                              double rho0, T *ret) {
+    const double u_in[3] = {ux, uy, uz};
+    for (long long i = gtid(); i < m; i += gstride()) {
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g[q] = g_all[q * m + i];
+        const T r = zou_he_node<T, QUASI, FACE>(g, kind, u_in, rho0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g_all[q * m + i] = g[q];
+        if (ret) ret[i] = r;
+    }
+}
+
+}  // namespace
+}  // namespace tlbm
+
+using namespace tlbm;
+
+extern "C" int tlbm_init_equilibrium(void *d_f, int dtype, int fluid, int table, int64_t t_n,
+                                     double rho, double ux, double uy, double uz, void *stream) {
+    if (t_n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, table, [&]<class T, int QU, int TB>() {
+        init_uniform_kernel<T, QU, TB><<<grid_capped(t_n * 64), 256, 0, as_stream(stream)>>>(
+            static_cast<T *>(d_f), t_n, rho, ux, uy, uz);
+        return launch_check("init_uniform_kernel");
+    });
+}
+
+extern "C" int tlbm_init_from_macroscopic(void *d_f, int dtype, int fluid, int table, int64_t t_n,
+                                          const void *d_rho, const void *d_u, void *stream) {
+    if (t_n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, table, [&]<class T, int QU, int TB>() {
+        init_fields_kernel<T, QU, TB><<<grid_capped(t_n * 64), 256, 0, as_stream(stream)>>>(
+            static_cast<T *>(d_f), t_n, static_cast<const T *>(d_rho),
+            static_cast<const T *>(d_u));
+        return launch_check("init_fields_kernel");
+    });
+}
+
+extern "C" int tlbm_to_canonical(const void *d_f, int dtype, int table, int64_t t_n,
+                                 void *d_canon, void *stream) {
+    if (t_n == 0) return TLBM_OK;
+    return dispatch(dtype, 0, table, [&]<class T, int QU, int TB>() {
+        canon_kernel<T, TB, true><<<grid_capped(t_n * 64), 256, 0, as_stream(stream)>>>(
+            static_cast<const T *>(d_f), static_cast<T *>(d_canon), t_n);
+        return launch_check("canon_kernel");
+    });
+}
+
+extern "C" int tlbm_from_canonical(const void *d_canon, int dtype, int table, int64_t t_n,
+                                   void *d_f, void *stream) {
+    if (t_n == 0) return TLBM_OK;
+    return dispatch(dtype, 0, table, [&]<class T, int QU, int TB>() {
+        canon_kernel<T, TB, false><<<grid_capped(t_n * 64), 256, 0, as_stream(stream)>>>(
+            static_cast<const T *>(d_canon), static_cast<T *>(d_f), t_n);
+        return launch_check("canon_kernel");
+    });
+}
+
+extern "C" int tlbm_macroscopic(const void *d_f, int dtype, int fluid, int table, int64_t t_n,
+                                void *d_rho, void *d_u, void *d_p, uint32_t *d_flags,
+                                void *stream) {
+    if (t_n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, table, [&]<class T, int QU, int TB>() {
+        macro_blocks_kernel<T, QU, TB><<<grid_capped(t_n * 64), 256, 0, as_stream(stream)>>>(
+            static_cast<const T *>(d_f), t_n, static_cast<T *>(d_rho), static_cast<T *>(d_u),
+            static_cast<T *>(d_p), d_flags);
+        return launch_check("macro_blocks_kernel");
+    });
+}
+
+extern "C" int tlbm_macroscopic_canonical(const void *d_f, int dtype, int fluid, int64_t n,
+                                          void *d_rho, void *d_u, void *d_p, uint32_t *d_flags,
+                                          void *stream) {
+    if (n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, 0, [&]<class T, int QU, int TB>() {
+        macro_canon_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+            static_cast<const T *>(d_f), n, static_cast<T *>(d_rho), static_cast<T *>(d_u),
+            static_cast<T *>(d_p), d_flags);
+        return launch_check("macro_canon_kernel");
+    });
+}
+
+extern "C" int tlbm_equilibrium(const void *d_rho, const void *d_u, int dtype, int fluid,
+                                int64_t n, void *d_feq, void *stream) {
+    if (n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, 0, [&]<class T, int QU, int TB>() {
+        equilibrium_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+            static_cast<const T *>(d_rho), static_cast<const T *>(d_u), n,
+            static_cast<T *>(d_feq));
+        return launch_check("equilibrium_kernel");
+    });
+}
+
+extern "C" int tlbm_collide_lbgk(void *d_f, int dtype, int fluid, int64_t n, double tau,
+                                 uint32_t *d_flags, void *stream) {
+    if (n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, 0, [&]<class T, int QU, int TB>() {
+        collide_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+            static_cast<T *>(d_f), n, 1.0 / tau, d_flags);
+        return launch_check("collide_kernel");
+    });
+}
+
+extern "C" int tlbm_zou_he(void *d_g, int dtype, int fluid, int face, int kind, int64_t m,
+                           double ux, double uy, double uz, double rho0, void *d_ret,
+                           void *stream) {
+    if (face < 0 || face > 5 || (kind != 0 && kind != 1)) {
+        set_error("tlbm_zou_he: face must be 0..5 and kind 0 (velocity) or 1 (pressure)");
+        return TLBM_ERR_ARG;
+    }
+    if (m == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, 0, [&]<class T, int QU, int TB>() {
+        auto *g = static_cast<T *>(d_g);
+        auto *r = static_cast<T *>(d_ret);
+        cudaStream_t s = as_stream(stream);
+        unsigned gr = grid_capped(m);
+        switch (face) {
+            case 0: zou_he_kernel<T, QU, 0><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+            case 1: zou_he_kernel<T, QU, 1><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+            case 2: zou_he_kernel<T, QU, 2><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+            case 3: zou_he_kernel<T, QU, 3><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+            case 4: zou_he_kernel<T, QU, 4><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+            default: zou_he_kernel<T, QU, 5><<<gr, 256, 0, s>>>(g, m, kind, ux, uy, uz, rho0, r); break;
+        }
+        return launch_check("zou_he_kernel");
+    });
+}

@@ -1,0 +1,193 @@
+// Node physics on register-resident populations g[19]: moments, LBGK
+// collision and the Zou-He face closures.
+//
+// Every expression keeps the reference's operation order (collision.py:46-130,
+// boundaries.py:132-195) and the library is compiled
+// with -fmad=false, so no multiply-add is contracted: with IEEE division and
+// square root (nvcc defaults) the results are bit-identical to the numpy
+// reference and to the C oracle, in both fp64 and fp32.
+//
+// All direction indices are compile-time after loop unrolling, so g[] stays
+// in registers (no local-memory indexing; checked with -Xptxas -v).
+#pragma once
+#include "d3q19.cuh"
+
+namespace tlbm {
+
+enum : uint32_t { ST_DIVERGED = 1u, ST_GUARD = 2u };
+
+// rho = ((g0 + g1) + ...) + g18; j_a accumulated from 0 in q order
+// (collision.py:55-72); u = j / rho (quasi) or j (incompressible)
+template <class T, int QUASI>
+__device__ __forceinline__ void moments(const T (&g)[Q], T &rho, T (&u)[3]) {
+    rho = g[0];
+#pragma unroll
+    for (int q = 1; q < Q; ++q) rho = rho + g[q];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (e_axis(q, a) == 1) acc = acc + g[q];
+            else if (e_axis(q, a) == -1) acc = acc - g[q];
+        }
+        u[a] = QUASI ? acc / rho : acc;
+    }
+}
+
+// collision.py:94-121 for one direction
+template <class T, int QUASI>
+__device__ __forceinline__ T equilibrium_q(int q, T rho, const T (&u)[3], T usq) {
+    T cu = T(0);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        if (e_axis(q, a) > 0) cu = cu + u[a];
+        else if (e_axis(q, a) < 0) cu = cu + (-u[a]);
+    }
+    T br = T(3.0) * cu + T(4.5) * cu * cu - T(1.5) * usq;
+    T w = T(weight(q));
+    return QUASI ? w * (rho * (T(1.0) + br)) : w * (rho + br);
+}
+
+template <class T>
+__device__ __forceinline__ T speed_sq(const T (&u)[3]) {
+    return u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+}
+
+template <class T, int QUASI>
+__device__ __forceinline__ uint32_t status_of(T rho, T usq, double u_guard) {
+    uint32_t st = 0;
+    if (rho != rho || (QUASI && !(rho > T(0)))) st |= ST_DIVERGED;
+    if (u_guard > 0.0 && sqrt((double)usq) > u_guard) st |= ST_GUARD;
+    return st;
+}
+
+// collide_lbgk in place: g <- g + fl(1/tau) (feq - g)  (collision.py:124-130)
+template <class T, int QUASI>
+__device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, double u_guard) {
+    T rho, u[3];
+    moments<T, QUASI>(g, rho, u);
+    T usq = speed_sq(u);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        T feq = equilibrium_q<T, QUASI>(q, rho, u, usq);
+        g[q] = g[q] + inv_tau * (feq - g[q]);
+    }
+    return status_of<T, QUASI>(rho, usq, u_guard);
+}
+
+// ---- Zou-He (boundaries.py:53-92 closures, 132-195 arithmetic) -----------
+// FACE = 2*axis + (0 low face, inward sign +1 | 1 high face, sign -1)
+__host__ __device__ constexpr int face_axis(int face) { return face >> 1; }
+__host__ __device__ constexpr int face_sign(int face) { return (face & 1) ? -1 : 1; }
+__host__ __device__ constexpr int c_dot_n(int q, int face) {
+    return e_axis(q, face_axis(face)) * face_sign(face);
+}
+// the unknown axis direction (c = n)
+__host__ __device__ constexpr int face_axis_dir(int face) {
+    return face == 0 ? 1 : face == 1 ? 3 : face == 2 ? 2 : face == 3 ? 4 : face == 4 ? 5 : 6;
+}
+// transverse axis of an unknown diagonal
+__host__ __device__ constexpr int diag_tau(int q, int face) {
+    return (face_axis(face) != 0 && ex(q) != 0) ? 0
+         : (face_axis(face) != 1 && ey(q) != 0) ? 1 : 2;
+}
+
+// ordered sum over the directions with c.n == cn and, if tau >= 0,
+// c_tau == sgn, in index order (boundaries.py:132-136)
+template <class T, int FACE>
+__device__ __forceinline__ T ordered_sum(const T (&g)[Q], int cn, int tau, int sgn) {
+    T acc = T(0);
+    bool first = true;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (c_dot_n(q, FACE) == cn && (tau < 0 || e_axis(q, tau) == sgn)) {
+            if (first) { acc = g[q]; first = false; }
+            else acc = acc + g[q];
+        }
+    }
+    return acc;
+}
+
+// _apply_closure (boundaries.py:179-195)
+template <class T, int FACE>
+__device__ __forceinline__ void zh_close(T (&g)[Q], const T (&j)[3]) {
+    constexpr int AX = face_axis(FACE);
+    constexpr int TQ = face_axis_dir(FACE);
+    const T third = T(1.0 / 3.0), sixth = T(1.0 / 6.0), half = T(0.5);
+    T jn = T(face_sign(FACE)) * j[AX];
+    g[TQ] = g[opp(TQ)] + third * jn;
+    T ntau[3];
+#pragma unroll
+    for (int tau = 0; tau < 3; ++tau) {
+        if (tau == AX) continue;
+        ntau[tau] = half * (ordered_sum<T, FACE>(g, 0, tau, 1) - ordered_sum<T, FACE>(g, 0, tau, -1))
+                  - third * j[tau];
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (c_dot_n(q, FACE) != 1 || q == TQ) continue;
+        const int tau = diag_tau(q, FACE);
+        const T s = T(e_axis(q, tau));
+        g[q] = g[opp(q)] + sixth * (jn + s * j[tau]) - s * ntau[tau];
+    }
+}
+
+// zou_he_velocity (boundaries.py:139-157)
+template <class T, int QUASI, int FACE>
+__device__ __forceinline__ void zh_velocity(T (&g)[Q], const double (&u_in)[3]) {
+    constexpr int AX = face_axis(FACE);
+    T u[3] = {T(u_in[0]), T(u_in[1]), T(u_in[2])};
+    T j[3];
+    if (QUASI) {
+        T un = T(face_sign(FACE)) * u[AX];
+        T k0 = ordered_sum<T, FACE>(g, 0, -1, 0);
+        T km = ordered_sum<T, FACE>(g, -1, -1, 0);
+        T rho = (k0 + T(2.0) * km) / (T(1.0) - un);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) j[a] = u[a] * rho;
+    } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) j[a] = u[a];
+    }
+    zh_close<T, FACE>(g, j);
+}
+
+// zou_he_pressure (boundaries.py:160-176)
+template <class T, int FACE>
+__device__ __forceinline__ void zh_pressure(T (&g)[Q], double rho0_in) {
+    constexpr int AX = face_axis(FACE);
+    T rho0 = T(rho0_in);
+    T k0 = ordered_sum<T, FACE>(g, 0, -1, 0);
+    T km = ordered_sum<T, FACE>(g, -1, -1, 0);
+    T jn = rho0 - (k0 + T(2.0) * km);
+    T j[3] = {T(0), T(0), T(0)};
+    j[AX] = T(face_sign(FACE)) * jn;
+    zh_close<T, FACE>(g, j);
+}
+
+template <class T, int QUASI>
+__device__ __forceinline__ void zou_he(T (&g)[Q], int tag, int face, const double (&u_in)[3],
+                                    double rho0) {
+    if (tag == INLET) {
+        switch (face) {
+            case 0: zh_velocity<T, QUASI, 0>(g, u_in); break;
+            case 1: zh_velocity<T, QUASI, 1>(g, u_in); break;
+            case 2: zh_velocity<T, QUASI, 2>(g, u_in); break;
+            case 3: zh_velocity<T, QUASI, 3>(g, u_in); break;
+            case 4: zh_velocity<T, QUASI, 4>(g, u_in); break;
+            default: zh_velocity<T, QUASI, 5>(g, u_in); break;
+        }
+    } else {
+        switch (face) {
+            case 0: zh_pressure<T, 0>(g, rho0); break;
+            case 1: zh_pressure<T, 1>(g, rho0); break;
+            case 2: zh_pressure<T, 2>(g, rho0); break;
+            case 3: zh_pressure<T, 3>(g, rho0); break;
+            case 4: zh_pressure<T, 4>(g, rho0); break;
+            default: zh_pressure<T, 5>(g, rho0); break;
+        }
+    }
+}
+
+}  // namespace tlbm

@@ -1,0 +1,172 @@
+// The fused D3Q19 step: pull gather through the neighbour-tile map, halfway
+// bounce-back fill, BB_WALL reflection, Zou-He inlet/outlet, LBGK collision
+// and the store into the other copy -- Alg. 2 of the paper
+// with the boundary contract of boundaries.py:1-28.
+//
+// Work mapping: one tile = 64 threads (2 warps, thread j <-> slot j, i.e. the
+// paper's x + 4y + 16z map, lattice.py:97-106); TILES_PER_CTA tiles per CTA.
+// Each thread issues its 19 loads back to back (one address select per
+// direction: neighbour slot if the link exists, else the node's own opposite
+// slot), so 19 independent 8-byte loads per thread are in flight.  Loads use
+// the read-only path (the source copy is immutable during the launch) and hit
+// L1 when the two warps of a tile share a sector.  With the B200 table every
+// 32-byte sector of the source copy is consumed by exactly one destination
+// tile, so DRAM traffic is the 2 x 19 x 8 B / node minimum plus metadata
+// (4 B/node meta word + 108 B/tile neighbour row).
+#include "common.cuh"
+#include "physics.cuh"
+
+namespace tlbm {
+namespace {
+
+template <class T>
+struct StepParams {
+    const T *__restrict__ src;
+    T *__restrict__ dst;
+    const int32_t *__restrict__ nbr;
+    const uint32_t *__restrict__ meta;
+    long long tile_begin, tile_end;
+    double inv_tau;
+    double inlet_u[3];
+    double outlet_rho;
+    double u_guard;
+    uint32_t *flags;
+};
+
+constexpr int TILE_VALUES = Q * 64;
+
+template <class T>
+__device__ __forceinline__ T load_ro(const T *p) { return __ldg(p); }
+
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC>
+__global__ void __launch_bounds__(64 * TPC)
+step_kernel(const StepParams<T> p) {
+    __shared__ int s_nbr[TPC][NBR];
+    const int ti = threadIdx.x >> 6;
+    const int j = threadIdx.x & 63;
+    const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
+    const long long tile = tile0 + ti;
+
+    if (VARIANT != TLBM_READ_WRITE_ONLY) {
+        for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
+            long long t = tile0 + i / NBR;
+            s_nbr[i / NBR][i % NBR] = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
+        }
+        __syncthreads();
+    }
+
+    const uint32_t meta = tile < p.tile_end ? p.meta[tile * 64 + j] : 0u;
+    uint32_t status = 0;
+    if (meta & META_ACTIVE) {
+        const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
+        const long long own = tile * TILE_VALUES;
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            long long off;
+            if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
+                off = own + q * 64 + slot_of<TABLE>(q, x, y, z);
+            } else {
+                const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
+                const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
+                const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
+                const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
+                const long long nb = (dx | dy | dz) ? (long long)s_nbr[ti][delta_index(dx, dy, dz)]
+                                                    : tile;
+                const long long pulled = nb * TILE_VALUES + q * 64
+                                       + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
+                const long long bounced = own + opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
+                off = ((meta >> q) & 1u) ? pulled : bounced;
+            }
+            g[q] = load_ro(p.src + off);
+        }
+
+        if (VARIANT == TLBM_FULL) {
+            const int tag = meta_type(meta);
+            if (tag == BB_WALL) {
+                // collision.py:250-252 reflect: f_new[q] = g[opp(q)]
+#pragma unroll
+                for (int q = 1; q < Q; ++q)
+                    if (q < opp(q)) { T t = g[q]; g[q] = g[opp(q)]; g[opp(q)] = t; }
+            } else {
+                if (tag == INLET || tag == OUTLET)
+                    zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
+                status = collide<T, QUASI>(g, T(p.inv_tau), p.u_guard);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) p.dst[own + q * 64 + slot_of<TABLE>(q, x, y, z)] = g[q];
+    }
+    if (p.flags) {
+        const uint32_t any = __reduce_or_sync(0xffffffffu, status);
+        if (any && (threadIdx.x & 31) == 0) atomicOr(p.flags, any);
+    }
+}
+
+constexpr int TPC = 4;
+
+template <class T, int QUASI, int TABLE, int VARIANT>
+int launch(const tlbm_step_args *a, cudaStream_t s) {
+    StepParams<T> p;
+    p.src = static_cast<const T *>(a->f_src);
+    p.dst = static_cast<T *>(a->f_dst);
+    p.nbr = a->nbr;
+    p.meta = a->meta;
+    p.tile_begin = a->tile_begin;
+    p.tile_end = a->tile_end;
+    p.inv_tau = 1.0 / a->tau;
+    for (int k = 0; k < 3; ++k) p.inlet_u[k] = a->inlet_u[k];
+    p.outlet_rho = a->outlet_rho;
+    p.u_guard = a->u_guard;
+    p.flags = a->flags;
+    const long long n = a->tile_end - a->tile_begin;
+    if (n <= 0) return TLBM_OK;
+    step_kernel<T, QUASI, TABLE, VARIANT, TPC>
+        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+    return launch_check("step_kernel");
+}
+
+struct StepLaunch {
+    const tlbm_step_args *a;
+    cudaStream_t s;
+    template <class T, int QUASI, int TABLE>
+    int operator()() const {
+        switch (a->variant) {
+            case TLBM_FULL: return launch<T, QUASI, TABLE, TLBM_FULL>(a, s);
+            case TLBM_PROPAGATION_ONLY:
+                return QUASI ? TLBM_OK : launch<T, 0, TABLE, TLBM_PROPAGATION_ONLY>(a, s);
+            case TLBM_READ_WRITE_ONLY:
+                return QUASI ? TLBM_OK : launch<T, 0, TABLE, TLBM_READ_WRITE_ONLY>(a, s);
+        }
+        set_error("unknown step variant %d", a->variant);
+        return TLBM_ERR_ARG;
+    }
+};
+
+}  // namespace
+}  // namespace tlbm
+
+using namespace tlbm;
+
+extern "C" int tlbm_step(const tlbm_step_args *a, void *stream) {
+    if (!a || !a->f_src || !a->f_dst || !a->meta ||
+        (a->variant != TLBM_READ_WRITE_ONLY && !a->nbr)) {
+        set_error("tlbm_step: null argument");
+        return TLBM_ERR_ARG;
+    }
+    if (a->f_src == a->f_dst) {
+        set_error("tlbm_step: source and destination copies must differ");
+        return TLBM_ERR_ARG;
+    }
+    if (a->tile_begin < 0 || a->tile_end > a->t_n || a->tile_begin > a->tile_end) {
+        set_error("tlbm_step: tile range [%lld, %lld) outside [0, %lld)",
+                  (long long)a->tile_begin, (long long)a->tile_end, (long long)a->t_n);
+        return TLBM_ERR_ARG;
+    }
+    if (!(a->tau > 0.5)) {
+        set_error("tlbm_step: relaxation time must exceed 0.5, got %g", a->tau);
+        return TLBM_ERR_ARG;
+    }
+    int fluid = (a->variant == TLBM_FULL) ? a->fluid : TLBM_INCOMPRESSIBLE;
+    return dispatch(a->dtype, fluid, a->table, StepLaunch{a, as_stream(stream)});
+}

@@ -1,0 +1,299 @@
+"""Solver: init, step and run of the tiled D3Q19 LBGK path on one GPU.
+
+The reference defines this module only in its SPEC (the
+step semantics are restated in SURVEY Appendix A).  API:
+
+``SimulationConfig``  SPEC.md:335-340 (collision, fluid, tau > 0.5,
+                      mrt_relaxation, precision f32|f64, u_max_guard=0.05),
+                      plus ``table`` (default LayoutTable.B200).
+``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,
+                      iteration, parity).
+``Solver``            owns the device state; ``step(n)``, ``run(n)``,
+                      ``macroscopic()``, ``fields_canonical()``.
+``step(state)`` / ``run(config, geometry, iterations, outputs)``  SPEC ops.
+
+Each step is one launch of the fused kernel (csrc/step.cu) reading copy
+``parity`` and writing copy ``1 - parity`` (A/B buffers);
+no host synchronisation happens between steps.  Divergence (NaN, or rho <= 0
+in the quasi-compressible model) and the |u| guard are OR-ed by the kernel
+into a per-iteration status word of a ring buffer; ``check()`` reads it and
+raises ``DivergenceError`` with the exact iteration.
+"""
+
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .collision import CollisionModel, DivergenceError, FluidModel, fluid_code
+from .geometry import Geometry
+from .layout import TABLE_CODE, FieldStore, LayoutTable
+from .lattice import Q, WEIGHTS
+from .tiling import DeviceTiling
+
+STATUS_RING = 4096
+
+
+class CompressibilityWarning(UserWarning):
+    """|u| exceeded SimulationConfig.u_max_guard."""
+
+
+@dataclass
+class SimulationConfig:
+    collision: CollisionModel = CollisionModel.LBGK
+    fluid: FluidModel = FluidModel.INCOMPRESSIBLE
+    tau: float = 0.6
+    mrt_relaxation: tuple = None
+    precision: str = "f64"
+    u_max_guard: float = 0.05
+    table: LayoutTable = LayoutTable.B200
+
+    def __post_init__(self):
+        self.collision = CollisionModel(getattr(self.collision, "value", self.collision))
+        self.fluid = FluidModel(getattr(self.fluid, "value", self.fluid))
+        self.table = LayoutTable(getattr(self.table, "value", self.table))
+        if not float(self.tau) > 0.5:
+            raise ValueError(f"relaxation time must exceed 0.5: {self.tau}")
+        if self.precision not in ("f32", "f64"):
+            raise ValueError(f"unknown precision: {self.precision!r}")
+        if self.collision is not CollisionModel.LBGK:
+            raise NotImplementedError("only LBGK collision is on the B200 path "
+                                      "(MRT is SURVEY section 8(f)-1 'next')")
+
+    @property
+    def dtype(self):
+        return np.float64 if self.precision == "f64" else np.float32
+
+
+@dataclass
+class SimulationState:
+    geometry: Geometry
+    tile_grid: object
+    field_store: FieldStore
+    iteration: int = 0
+    parity: int = 0
+    config: SimulationConfig = None
+    solver: object = field(default=None, repr=False)
+
+
+class Solver:
+    """Device-resident tiled LBGK solver for one geometry on one GPU."""
+
+    def __init__(self, geometry, config=None, device=None, tiling=None):
+        self.config = config if config is not None else SimulationConfig()
+        self.geometry = geometry
+        self.tiling = tiling if tiling is not None else DeviceTiling(geometry, device)
+        self.device = self.tiling.device
+        self.t_n = self.tiling.t_n
+        self.n_fn = self.tiling.n_fn
+        self.store = FieldStore(self.t_n, self.config.table, self.config.dtype, self.device)
+        self.code = self.store.code
+        self.fluid = fluid_code(self.config.fluid)
+        self.table = TABLE_CODE[self.config.table]
+        self.iteration = 0
+        self.parity = 0
+        self._checked = 0
+        self.guard_iterations = []
+        self.status = torch.zeros(STATUS_RING, dtype=torch.int32, device=self.device)
+        self._grid = None
+        self._args = nat.StepArgs()
+        a = self._args
+        a.dtype, a.fluid, a.table, a.variant = self.code, self.fluid, self.table, nat.FULL
+        a.t_n, a.tile_begin, a.tile_end = self.t_n, 0, self.t_n
+        a.nbr = self.tiling.nbr.data_ptr()
+        a.meta = self.tiling.meta.data_ptr()
+        a.tau = float(self.config.tau)
+        a.inlet_u[:] = list(geometry.inlet_velocity)
+        a.outlet_rho = float(geometry.outlet_density)
+        a.u_guard = float(self.config.u_max_guard or 0.0)
+        self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
+        self.init_equilibrium()
+
+    # -- initial state -------------------------------------------------------
+    def init_equilibrium(self, rho=1.0, u=(0.0, 0.0, 0.0)):
+        """Both copies, all 64 slots of every tile := equilibrium(rho, u)
+        (the conventional cold start uses rho=1, u=0)."""
+        nat.require_cuda(self.device)
+        for c in (0, 1):
+            nat.call("tlbm_init_equilibrium", nat.ptr(self.store.copy_tensor(c)), self.code,
+                     self.fluid, self.table, self.t_n, float(rho), *(float(v) for v in u),
+                     nat.stream_ptr(self.device))
+        self._reset_counters()
+
+    def init_from_macroscopic(self, rho, u):
+        """Both copies := equilibrium(rho, u) per slot; rho (t_n, 64), u
+        (3, t_n, 64) canonical arrays (numpy or CUDA tensors)."""
+        nat.require_cuda(self.device)
+        dt = self.store.tdtype
+        r = torch.as_tensor(rho).to(self.device, dt).contiguous()
+        v = torch.as_tensor(u).to(self.device, dt).contiguous()
+        if tuple(r.shape) != (self.t_n, 64) or tuple(v.shape) != (3, self.t_n, 64):
+            raise ValueError("expected rho (t_n, 64) and u (3, t_n, 64)")
+        for c in (0, 1):
+            nat.call("tlbm_init_from_macroscopic", nat.ptr(self.store.copy_tensor(c)),
+                     self.code, self.fluid, self.table, self.t_n, nat.ptr(r), nat.ptr(v),
+                     nat.stream_ptr(self.device))
+        self._reset_counters()
+
+    def set_fields_canonical(self, values, copy=None):
+        """Overwrite a copy (default: both) from (19, t_n, 64) canonical values."""
+        for c in ((0, 1) if copy is None else (copy,)):
+            self.store.fill_canonical(c, values)
+
+    def _reset_counters(self):
+        self.iteration = 0
+        self.parity = 0
+        self._checked = 0
+        self.guard_iterations = []
+        self.status.zero_()
+
+    # -- stepping ------------------------------------------------------------
+    def step(self, n=1, variant=nat.FULL, check=True):
+        """Advance n iterations (no host sync unless ``check`` and the status
+        ring is full or n is exhausted)."""
+        nat.require_cuda(self.device)
+        a = self._args
+        a.variant = int(variant)
+        stream = nat.stream_ptr(self.device)
+        lib = nat.load()
+        base = self.status.data_ptr()
+        for _ in range(int(n)):
+            if self.iteration - self._checked >= STATUS_RING:
+                self.check()
+            a.f_src = self._copies[self.parity]
+            a.f_dst = self._copies[1 - self.parity]
+            a.flags = base + 4 * (self.iteration % STATUS_RING)
+            rc = lib.tlbm_step(nat.ctypes.byref(a), stream)
+            if rc:
+                nat.check(rc)
+            self.parity ^= 1
+            self.iteration += 1
+        if check:
+            self.check()
+        return self
+
+    def check(self):
+        """Read the status ring; raise DivergenceError at the first divergent
+        iteration, record |u| guard trips (CompressibilityWarning)."""
+        pending = self.iteration - self._checked
+        if pending <= 0:
+            return
+        st = self.status.cpu().numpy()
+        for it in range(self._checked, self.iteration):
+            w = int(st[it % STATUS_RING])
+            if w & nat.FLAG_GUARD:
+                self.guard_iterations.append(it)
+            if w & nat.FLAG_DIVERGED:
+                self.status.zero_()
+                self._checked = self.iteration
+                raise DivergenceError("simulation diverged (NaN or non-positive density)",
+                                      iteration=it)
+        if st.any():
+            self.status.zero_()
+        if self.guard_iterations and self.guard_iterations[-1] >= self._checked:
+            warnings.warn(f"|u| exceeded u_max_guard={self.config.u_max_guard} at iteration "
+                          f"{self.guard_iterations[-1]}", CompressibilityWarning, stacklevel=2)
+        self._checked = self.iteration
+
+    def run(self, iterations, check_every=STATUS_RING):
+        left = int(iterations)
+        while left > 0:
+            k = min(left, check_every)
+            self.step(k, check=True)
+            left -= k
+        return self
+
+    # -- readout -------------------------------------------------------------
+    def macroscopic(self, device=False, copy=None):
+        """(rho (t_n,64), u (3,t_n,64), p (t_n,64)) of the current copy, in
+        canonical slot order (collision.py:75-91 on read_canonical)."""
+        nat.require_cuda(self.device)
+        c = self.parity if copy is None else copy
+        dt = self.store.tdtype
+        rho = torch.empty((self.t_n, 64), dtype=dt, device=self.device)
+        u = torch.empty((3, self.t_n, 64), dtype=dt, device=self.device)
+        p = torch.empty((self.t_n, 64), dtype=dt, device=self.device)
+        flags = torch.zeros(1, dtype=torch.int32, device=self.device)
+        nat.call("tlbm_macroscopic", nat.ptr(self.store.copy_tensor(c)), self.code, self.fluid,
+                 self.table, self.t_n, nat.ptr(rho), nat.ptr(u), nat.ptr(p), nat.ptr(flags),
+                 nat.stream_ptr(self.device))
+        if self.fluid == nat.QUASI and int(flags.item()) & nat.FLAG_DIVERGED:
+            raise DivergenceError("non-positive density in quasi-compressible flow",
+                                  iteration=self.iteration)
+        if device:
+            return rho, u, p
+        return rho.cpu().numpy(), u.cpu().numpy(), p.cpu().numpy()
+
+    def fields_canonical(self, copy=None, device=False):
+        """(19, t_n, 64) canonical populations of the current (or given) copy."""
+        return self.store.read_canonical(self.parity if copy is None else copy, device=device)
+
+    @property
+    def tile_grid(self):
+        if self._grid is None:
+            self._grid = self.tiling.grid()
+        return self._grid
+
+    def nonsolid_mask(self, device=False):
+        m = (self.tiling.meta & 1).bool()
+        return m if device else m.cpu().numpy()
+
+    def total_mass(self):
+        """Sum of rho over non-solid slots (fp64 accumulation on the GPU)."""
+        rho, _, _ = self.macroscopic(device=True)
+        return float(rho[self.nonsolid_mask(device=True)].double().sum().item())
+
+    def to_dense(self, canonical):
+        """Scatter a (..., t_n, 64) canonical array to (..., nx, ny, nz) on the
+        GPU (absent tiles / padding dropped; absent tiles read as 0)."""
+        x = torch.as_tensor(canonical, device=self.device)
+        lead = tuple(x.shape[:-2])
+        pd = tuple(m * 4 for m in self.tiling.mesh)
+        out = torch.zeros(lead + pd, dtype=x.dtype, device=self.device)
+        ne = self.tiling.non_empty.long()
+        s = torch.arange(64, device=self.device)
+        xi = ne[:, 0:1] + (s & 3)
+        yi = ne[:, 1:2] + ((s >> 2) & 3)
+        zi = ne[:, 2:3] + (s >> 4)
+        out[..., xi, yi, zi] = x
+        nx, ny, nz = self.tiling.dims
+        return out[..., :nx, :ny, :nz]
+
+    @property
+    def state(self):
+        return SimulationState(self.geometry, self.tile_grid, self.store, self.iteration,
+                               self.parity, self.config, self)
+
+
+def init_state(config, geometry, device=None):
+    """Solver init: tiling, two-copy store, equilibrium start."""
+    return Solver(geometry, config, device).state
+
+
+def step(state):
+    """One LBM iteration; returns the updated state."""
+    s = state.solver
+    if s is None:
+        raise ValueError("state has no solver attached; build it with init_state()")
+    s.step(1)
+    state.iteration, state.parity = s.iteration, s.parity
+    return state
+
+
+def run(config, geometry, iterations, outputs=None, device=None, check_every=STATUS_RING):
+    """Iterate ``iterations`` steps.  Returns
+    (state, diagnostics) with MFLUPS-relevant counts and guard trips.
+    ``outputs``: optional callable(solver) invoked after the run."""
+    solver = Solver(geometry, config, device)
+    solver.run(iterations, check_every=check_every)
+    diagnostics = {"iterations": solver.iteration, "t_n": solver.t_n, "n_fn": solver.n_fn,
+                   "guard_iterations": list(solver.guard_iterations)}
+    if outputs is not None:
+        outputs(solver)
+    return solver.state, diagnostics
+
+
+def rest_weights(dtype=np.float64):
+    return WEIGHTS.astype(dtype)

@@ -1,0 +1,108 @@
+"""GPU: the device tiler is bit-exact with the reference's build_tiling,
+_neighbor_indices and per-tile counts (golden vectors made by the reference,
+plus the oracle restatement on further geometries)."""
+
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import tiling as ot
+from paper_1611_02445_b200 import geometry as geo_mod
+from paper_1611_02445_b200 import tiling
+
+pytestmark = pytest.mark.gpu
+D27 = list(itertools.product((-1, 0, 1), repeat=3))
+
+
+def _check(g, types, tm_ref, ne_ref, nbr_ref=None, counts_ref=None, periodic=(False,) * 3):
+    grid = tiling.build_tiling(g)
+    assert grid.tile_map.dtype == np.int32 and grid.non_empty.dtype == np.int32
+    assert np.array_equal(grid.tile_map, tm_ref)
+    assert np.array_equal(grid.non_empty, ne_ref)
+    if nbr_ref is None:
+        nbr_ref = ot.neighbor_indices(tm_ref, ne_ref, D27, periodic)
+    assert np.array_equal(grid.device.nbr.cpu().numpy(), nbr_ref)
+    if counts_ref is None:
+        counts_ref = ot.nonsolid_blocks(types, ne_ref).sum(1)
+    assert np.array_equal(tiling.per_tile_nonsolid_counts(grid, g), counts_ref)
+    meta = grid.device.meta.cpu().numpy()
+    assert np.array_equal((meta & 1).astype(bool), ot.nonsolid_blocks(types, ne_ref))
+    assert np.array_equal((meta >> 19) & 7, ot.tile_types(types, ne_ref))
+    return grid
+
+
+def test_golden_tilings(golden):
+    gd = golden("tiling")
+    names = sorted({k.rsplit("_", 1)[0] for k in gd if k.endswith("_types")})
+    for name in names:
+        types = gd[f"{name}_types"]
+        g = geo_mod.Geometry(types)
+        _check(g, types, gd[f"{name}_tile_map"], gd[f"{name}_non_empty"], gd[f"{name}_nbr"],
+               gd[f"{name}_counts"])
+
+
+@pytest.mark.parametrize("shape", [(4, 4, 4), (5, 9, 3), (1, 1, 1), (33, 17, 21), (64, 8, 130)])
+def test_random_tilings(shape):
+    rng = np.random.default_rng(sum(shape))
+    for density in (0.02, 0.3, 0.9):
+        types = (rng.random(shape) < density).astype(np.uint8)
+        g = geo_mod.Geometry(types)
+        tm, ne = ot.build_tiling(types)
+        if len(ne) == 0:
+            grid = tiling.build_tiling(g)
+            assert grid.t_n == 0 and np.all(grid.tile_map == -1)
+            continue
+        _check(g, types, tm, ne)
+
+
+def test_all_solid():
+    grid = tiling.build_tiling(geo_mod.Geometry(np.zeros((9, 4, 6), np.uint8)))
+    assert grid.t_n == 0
+    assert grid.tile_map.shape == (3, 1, 2) and np.all(grid.tile_map == -1)
+
+
+def test_cavity100_tile_count():
+    """SPEC tiling example: cavity3d(100) -> t_n = 25^3 = 15625."""
+    g = geo_mod.generate_cavity3d(100)
+    grid = tiling.build_tiling(g)
+    assert grid.t_n == 15625
+    st = tiling.tile_utilization(grid, g)
+    assert st.n_fn == 100 ** 3 and st.eta_t == 1.0
+
+
+def test_periodic_neighbors():
+    g = geo_mod.generate_channel("square", 12, axis=0, length=16, ends="periodic")
+    types = g.types
+    tm, ne = ot.build_tiling(types)
+    _check(g, types, tm, ne, periodic=g.periodic)
+
+
+def test_sphere_pack_counts():
+    g = geo_mod.generate_sphere_pack(48, 12, 0.5, seed=1234)
+    types = g.types
+    tm, ne = ot.build_tiling(types)
+    grid = _check(g, types, tm, ne)
+    st = tiling.tile_utilization(grid, g)
+    assert st.n_fn == g.nonsolid_count()
+
+
+def test_utilization_matches_reference(reference, golden):
+    rt, rg = reference.tiling, reference.geometry
+    for b in (10, 13):
+        a = rg.generate_cavity3d(b)
+        ref = rt.tile_utilization(rt.build_tiling(a), a)
+        g = geo_mod.generate_cavity3d(b)
+        got = tiling.tile_utilization(tiling.build_tiling(g), g)
+        assert (got.t_n, got.n_fn, got.eta_t, got.eta_f, got.eta_e) == \
+            (ref.t_n, ref.n_fn, ref.eta_t, ref.eta_f, ref.eta_e)
+
+
+def test_rejects_bad_faces():
+    t = np.ones((8, 8, 8), np.uint8)
+    t[0, 0, 0] = 3          # inlet on a corner: three faces
+    with pytest.raises(ValueError):
+        tiling.build_tiling(geo_mod.Geometry(t))
+    t[0, 0, 0] = 9          # unknown tag
+    with pytest.raises(ValueError):
+        tiling.build_tiling(geo_mod.Geometry(t))

@@ -1,0 +1,82 @@
+"""CPU checks of libtlbm.so without a GPU: it loads, exports every symbol
+include/tlbm.h declares, and its compiled-in lattice/layout tables equal the
+reference's (golden) and the Python mirror's."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1611_02445_b200 import _native as nat
+from paper_1611_02445_b200 import lattice, layout
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "tlbm.h")).read()
+    return sorted(set(re.findall(r"\b(tlbm_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_matches_binding():
+    assert header_symbols() == sorted(nat.EXPORTED)
+
+
+def test_library_exports_all_symbols():
+    lib = nat.load()
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+    assert lib.tlbm_abi_version() == nat.ABI_VERSION
+
+
+def test_library_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", nat.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("table", list(layout.LayoutTable))
+def test_compiled_tables(golden, table):
+    e, o, w, p = nat.lattice_tables(layout.TABLE_CODE[table])
+    g = golden("lattice")
+    assert np.array_equal(e, g["e"]) and np.array_equal(o, g["opp"])
+    assert np.array_equal(w, g["w"])
+    assert np.array_equal(p, layout.table_permutations(table))
+    if table.value in ("xyz", "optimized"):
+        assert np.array_equal(p, g[f"perm_{table.value}"])
+
+
+def test_python_lattice_matches_golden(golden):
+    g = golden("lattice")
+    assert np.array_equal(lattice.E_VECTORS, g["e"])
+    assert np.array_equal(lattice.OPPOSITE, g["opp"])
+    assert np.array_equal(lattice.WEIGHTS, g["w"])
+    assert sum(lattice.WEIGHTS_EXACT) == 1
+
+
+def test_layouts_bijective():
+    """SPEC acceptance 3 (plus the ZXY kind)."""
+    for kind in layout.LayoutKind:
+        assert sorted(layout.offsets(kind)) == list(range(64))
+
+
+def test_value_address_matches_reference(reference):
+    rl = reference.layout
+    for t in ("optimized", "xyz"):
+        for args in [(0, 0, 0, 1, 2, 3), (5, 7, 1, 3, 3, 0), (9, 18, 1, 0, 1, 2)]:
+            a = rl.value_address(*args, t_n=10, table=rl.LayoutTable(t))
+            b = layout.value_address(*args, t_n=10, table=layout.LayoutTable(t))
+            assert a == b
+
+
+def test_error_reporting_without_gpu():
+    # argument validation happens before any CUDA call
+    rc = nat.load().tlbm_lattice_tables(7, None, None, None, None)
+    assert rc == 1
+    assert b"layout table" in nat.load().tlbm_last_error()
+
+
+def test_tiling_scratch_size():
+    assert nat.load().tlbm_tiling_scratch_bytes(64, 64, 64) >= 16 ** 3
