@@ -148,7 +148,7 @@ def cpu_oracle_mlups(precision, n, seconds, threads=0):
     dt = np.float64 if precision == "f64" else np.float32
     length = 32
     geo = workloads.channel(n, length=length)
-    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.05, 0.0, 0.0))
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.04, 0.0, 0.0))
     cores = threads or len(os.sched_getaffinity(0))
     o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
                              f0=f0, dtype=dt, nthreads=cores)
@@ -177,7 +177,7 @@ def run_reference(args):
     dt = np.float64 if args.precision == "f64" else np.float32
     length = 32
     geo = workloads.channel(args.n, length=length)
-    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.05, 0.0, 0.0))
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.04, 0.0, 0.0))
     cores = len(os.sched_getaffinity(0))
     o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
                              f0=f0, dtype=dt, nthreads=cores)
@@ -232,7 +232,7 @@ def e2e_run(args, torch, geo_host):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = sv.Solver(geo_host, cfg)
-    s.init_equilibrium(1.0, (0.05, 0.0, 0.0))
+    s.init_equilibrium(1.0, (0.04, 0.0, 0.0))
     for i in range(args.steps):
         s.step(1, check=False)
         slot = (s.iteration - 1) % sv.STATUS_RING

@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtlbm.so")
+LIB_PATH = os.environ.get("TLBM_LIB") or os.path.join(HERE, "lib", "libtlbm.so")
 ABI_VERSION = 1
 
 F64, F32 = 0, 1

@@ -149,14 +149,16 @@ class FieldStore:
     """Two copies of all f_q in per-tile 64-slot blocks, resident on the GPU
     (layout.py:135-167).  ``flat`` is a torch tensor of 2*t_n*19*64 values."""
 
-    def __init__(self, t_n, table=LayoutTable.OPTIMIZED, dtype=np.float64, device=None):
+    def __init__(self, t_n, table=LayoutTable.OPTIMIZED, dtype=np.float64, device=None,
+                 zero=True):
         self.device = nat.require_cuda(device)
         self.t_n = int(t_n)
         self.table = table
         self.dtype = np.dtype(dtype)
         self.code = nat.code_of(self.dtype)
         self.tdtype = nat.torch_dtype(self.code)
-        self.flat = torch.zeros(2 * self.t_n * Q * 64, dtype=self.tdtype, device=self.device)
+        alloc = torch.zeros if zero else torch.empty   # Solver overwrites every slot
+        self.flat = alloc(2 * self.t_n * Q * 64, dtype=self.tdtype, device=self.device)
         self.perms = table_permutations(table)
 
     def copy_tensor(self, copy):

@@ -88,7 +88,8 @@ class Solver:
         self.device = self.tiling.device
         self.t_n = self.tiling.t_n
         self.n_fn = self.tiling.n_fn
-        self.store = FieldStore(self.t_n, self.config.table, self.config.dtype, self.device)
+        self.store = FieldStore(self.t_n, self.config.table, self.config.dtype, self.device,
+                                zero=False)
         self.code = self.store.code
         self.fluid = fluid_code(self.config.fluid)
         self.table = TABLE_CODE[self.config.table]

@@ -5,7 +5,7 @@ Seeds are fixed; tau = 0.6; LBGK incompressible unless noted.
 cavity(64)          config 1: lid-driven cavity, lid u = (0.05, 0, 0)
 channel(256)        config 2: square channel d = 256 along x, bounce-back
                     ring on the y/z faces, periodic in x (extension); started
-                    from equilibrium(rho, u) with u = (0.05, 0, 0) and a seeded
+                    from equilibrium(rho, u) with u = (0.04, 0, 0) and a seeded
                     +/-1e-3 perturbation of rho and u so the flow evolves
 sphere_pack(p)      config 3: generate_sphere_pack(256, 40, p, seed=1234,
                     flow_axis=2, inlet u = (0, 0, 0.01)); p = 1.0 -> all-fluid
@@ -41,7 +41,7 @@ def vessel_tree(shape=(512, 512, 1024), seed=1234):
     return geometry.generate_vessel_tree(shape, seed=seed)
 
 
-def perturbed_fields(t_n, dtype, device, u0=(0.05, 0.0, 0.0), amp=1e-3, seed=1234):
+def perturbed_fields(t_n, dtype, device, u0=(0.04, 0.0, 0.0), amp=1e-3, seed=1234):
     """(rho, u) canonical fields: rho = 1 + e, u = u0 + e, e ~ U(-amp, amp)."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
@@ -53,7 +53,7 @@ def perturbed_fields(t_n, dtype, device, u0=(0.05, 0.0, 0.0), amp=1e-3, seed=123
 
 
 def make_solver(geo, precision="f64", fluid="incompressible", table="b200", perturb=True,
-                device=None, u0=(0.05, 0.0, 0.0)):
+                device=None, u0=(0.04, 0.0, 0.0)):
     cfg = SimulationConfig(fluid=fluid, tau=TAU, precision=precision, table=table)
     s = Solver(geo, cfg, device=device)
     if perturb:

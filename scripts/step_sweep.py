@@ -1,0 +1,47 @@
+"""Time the step kernel variants (full / propagation-only / read-write-only)
+on a workload; prints one JSON line per (variant).  Used for tuning runs on
+the GPU box: TLBM_LIB selects an alternative build of libtlbm.so."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1611_02445_b200 import _native as nat  # noqa: E402
+from paper_1611_02445_b200 import workloads  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--n", type=int, default=256)
+p.add_argument("--precision", default="f64")
+p.add_argument("--table", default="b200")
+p.add_argument("--steps", type=int, default=100)
+p.add_argument("--variants", default="full,prop,rw")
+p.add_argument("--geometry", default="channel")
+p.add_argument("--porosity", type=float, default=0.5)
+a = p.parse_args()
+if a.geometry == "channel":
+    geo = workloads.channel(a.n)
+elif a.geometry == "cavity":
+    geo = workloads.cavity(a.n)
+else:
+    geo = workloads.sphere_pack(a.porosity, n=a.n)
+s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0))
+vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY}
+n_d = 8 if a.precision == "f64" else 4
+for v in a.variants.split(","):
+    s.step(5, variant=vmap[v], check=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    s.step(a.steps, variant=vmap[v], check=False)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    mlups = s.n_fn / (ms / 1e3) / 1e6
+    gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
+    print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "geometry": a.geometry, "n": a.n,
+                      "precision": a.precision, "table": a.table, "variant": v,
+                      "ms": round(ms, 4), "mlups": round(mlups, 1), "gbs": round(gbs, 1),
+                      "frac": round(gbs / 6533.5, 4), "n_fn": s.n_fn, "t_n": s.t_n}), flush=True)
