@@ -3,14 +3,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 
 N = 1 workload: BASELINE config 2 -- dense square channel 256^3, bounce-back
-ring, periodic along x, LBGK incompressible, fp64, tau = 0.6, started from a
+ring, periodic along its axis z, LBGK incompressible, fp64, tau = 0.6, started from a
 perturbed equilibrium (paper_1611_02445_b200/workloads.py).  One "step" = one
 launch of the fused collide+propagate kernel over all 262,144 tiles.  The
 field (2 x 2.55 GB) is far larger than L2 (126 MB), so no flush is needed.
 
 N > 1 (torchrun, one rank per GPU): weak scaling -- every rank owns a
-256^3 z-slab of a 256 x 256 x 256N periodic-x channel; ghost tile layers are
-exchanged every step over NCCL (paper_1611_02445_b200/slabs.py).
+256^3 z-slab of a 256 x 256 x 256N channel periodic in z; the boundary tile
+layers' outgoing z planes are exchanged every step over NCCL, overlapped with
+the interior-tile launch (paper_1611_02445_b200/slabs.py).
 
 Reported (one JSON line on rank 0):
   value      MLUPS over all ranks (non-solid node updates / s / 1e6), device
@@ -147,8 +148,8 @@ def cpu_oracle_mlups(precision, n, seconds, threads=0):
     from paper_1611_02445_b200 import workloads
     dt = np.float64 if precision == "f64" else np.float32
     length = 32
-    geo = workloads.channel(n, length=length)
-    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.04, 0.0, 0.0))
+    geo = workloads.channel_z(n, length=length)
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.0, 0.0, 0.04))
     cores = threads or len(os.sched_getaffinity(0))
     o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
                              f0=f0, dtype=dt, nthreads=cores)
@@ -163,7 +164,7 @@ def cpu_oracle_mlups(precision, n, seconds, threads=0):
             break
     return {"value": n_fn * steps / el / 1e6, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"C oracle (oracle/tlbm_oracle.c, OpenMP x{cores}) on the channel "
-                      f"{length}x{n}x{n} slab (periodic x), {precision}, {steps} steps "
+                      f"{n}x{n}x{length} slab (periodic z), {precision}, {steps} steps "
                       f"in {el:.1f} s"}
 
 
@@ -176,8 +177,8 @@ def run_reference(args):
     from paper_1611_02445_b200 import workloads
     dt = np.float64 if args.precision == "f64" else np.float32
     length = 32
-    geo = workloads.channel(args.n, length=length)
-    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.04, 0.0, 0.0))
+    geo = workloads.channel_z(args.n, length=length)
+    f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.0, 0.0, 0.04))
     cores = len(os.sched_getaffinity(0))
     o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
                              f0=f0, dtype=dt, nthreads=cores)
@@ -191,7 +192,7 @@ def run_reference(args):
     total = sum(t_all)
     value = n_fn * args.steps / total / 1e6
     sample = (f"C oracle port (oracle/tlbm_oracle.c, OpenMP x{cores}): each step = one full "
-              f"step of the channel {length}x{args.n}x{args.n} slab (periodic x), "
+              f"step of the channel {args.n}x{args.n}x{length} slab (periodic z), "
               f"{args.precision}; the reference has no step of its own (SURVEY 0.2)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
@@ -208,20 +209,6 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU arm
-def timed_steps(solver, steps, torch):
-    """K steps bracketed by synchronize + CUDA events on the launching
-    stream; returns elapsed ms."""
-    stream = torch.cuda.current_stream()
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    start.record(stream)
-    solver.step(steps, check=False)
-    end.record(stream)
-    torch.cuda.synchronize()
-    return start.elapsed_time(end)
-
-
 def e2e_run(args, torch, geo_host):
     """Public API end to end from host data: Solver(geometry) [H2D of the
     tags, device tiler + metadata, init], K x step() each with an async D2H of
@@ -232,7 +219,7 @@ def e2e_run(args, torch, geo_host):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = sv.Solver(geo_host, cfg)
-    s.init_equilibrium(1.0, (0.04, 0.0, 0.0))
+    s.init_equilibrium(1.0, (0.0, 0.0, 0.04))
     for i in range(args.steps):
         s.step(1, check=False)
         slot = (s.iteration - 1) % sv.STATUS_RING
@@ -264,19 +251,11 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        from paper_1611_02445_b200 import slabs
-        runner = slabs.SlabChannel(args.n, world, rank, precision=args.precision,
-                                   table=args.table)
-        n_fn_rank = runner.n_fn_owned
-        step_fn = runner.step
-        sync_all = runner.barrier
-    else:
-        geo = workloads.channel(args.n)
-        solver = workloads.make_solver(geo, precision=args.precision, table=args.table)
-        n_fn_rank = solver.n_fn
-        step_fn = lambda k: solver.step(k, check=False)  # noqa: E731
-        sync_all = lambda: None  # noqa: E731
-        runner = solver
+    from paper_1611_02445_b200 import slabs
+    runner = slabs.SlabChannel(args.n, world, rank, precision=args.precision, table=args.table)
+    n_fn_rank = runner.n_fn_owned
+    step_fn = runner.step
+    sync_all = runner.barrier
 
     for _ in range(args.warmup):
         step_fn(1)
@@ -304,8 +283,7 @@ def run_b200(args):
     else:
         n_fn_total = n_fn_rank
     # divergence check outside the timed region
-    if world == 1:
-        solver.check()
+    runner.slab.solver.check()
 
     ms_step = ms / args.steps
     value = n_fn_total * args.steps / (ms / 1e3) / 1e6
@@ -322,8 +300,10 @@ def run_b200(args):
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
         "config": {"workload": f"channel{args.n}_periodic_{args.precision}"
                                + (f"_slab_x{world}" if world > 1 else ""),
-                   "geometry": f"square channel d={args.n}, BB ring, periodic x, "
-                               f"{args.n}x{args.n}x{args.n} per GPU",
+                   "geometry": f"square channel d={args.n} along z, BB ring, periodic z, "
+                               f"{args.n}x{args.n}x{args.n} per GPU"
+                               + (f", global {args.n}x{args.n}x{args.n * world}"
+                                  if world > 1 else ""),
                    "model": "LBGK incompressible, tau=0.6", "layout_table": args.table,
                    "n_fn_per_gpu": n_fn_rank, "t_n_per_gpu": n_fn_rank // 64,
                    "l2": "inputs larger than L2 (field %.2f GB per copy)"
@@ -339,9 +319,9 @@ def run_b200(args):
         "gpu_launches": args.steps,
     }
     if rank == 0 and world == 1 and not args.no_e2e:
-        del runner, solver
+        del runner
         torch.cuda.empty_cache()
-        line["e2e"] = e2e_run(args, torch, workloads.channel(args.n))
+        line["e2e"] = e2e_run(args, torch, workloads.channel_z(args.n))
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_mlups(args.precision, args.n, args.cpu_seconds)
     if rank == 0:

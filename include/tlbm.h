@@ -123,6 +123,14 @@ int tlbm_zou_he(void *d_g, int dtype, int fluid, int face, int kind, int64_t m,
                 double ux, double uy, double uz, double rho0, void *d_ret,
                 void *stream);
 
+/* Slab halo of a z decomposition: pack (pack=1) the outer z
+ * plane of tiles [tile_begin, tile_end) of one copy for the 5 directions
+ * leaving it upward (up=1: T NT ST ET WT, plane z=3) or downward (up=0:
+ * B NB SB EB WB, plane z=0) into d_buf (80 values per tile), or unpack
+ * (pack=0) d_buf into the same slots of ghost tiles. */
+int tlbm_halo(void *d_f, int dtype, int table, int64_t tile_begin,
+              int64_t tile_end, int up, int pack, void *d_buf, void *stream);
+
 /* ---- the step (Alg. 2; boundaries.py:1-28) ------------- */
 typedef struct {
     int dtype, fluid, table, variant;

@@ -60,6 +60,7 @@ _PROTOS = {
     "tlbm_collide_lbgk": (c_int, [c_vp, c_int, c_int, c_i64, c_dbl, c_vp, c_vp]),
     "tlbm_zou_he": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_i64, c_dbl, c_dbl,
                             c_dbl, c_dbl, c_vp, c_vp]),
+    "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
 }
 

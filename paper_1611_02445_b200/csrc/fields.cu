@@ -285,3 +285,62 @@ extern "C" int tlbm_zou_he(void *d_g, int dtype, int fluid, int face, int kind, 
         return launch_check("zou_he_kernel");
     });
 }
+
+// ---- slab halo (multi-GPU z decomposition) --------------------
+// A rank's boundary tile layer sends, per tile, the 16 nodes of its outer z
+// plane for the 5 directions that cross it: up (e_z = +1: T, NT, ST, ET, WT)
+// from plane z = 3, down (e_z = -1: B, NB, SB, EB, WB) from plane z = 0.
+// Packed layout: buf[(tile - tile_begin) * 80 + k * 16 + (x + 4 y)].
+namespace tlbm {
+namespace {
+
+__host__ __device__ constexpr int halo_dir(int up, int k) {
+    return up ? (k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 13 : k == 3 ? 15 : 17)
+              : (k == 0 ? 6 : k == 1 ? 12 : k == 2 ? 14 : k == 3 ? 16 : 18);
+}
+
+template <class T, int TABLE, int UP, bool PACK>
+__global__ void halo_kernel(T *f, long long tile_begin, long long n_tiles, T *buf) {
+    const long long n = n_tiles * 80;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        const long long t = i / 80;
+        const int r = (int)(i % 80);
+        const int k = r >> 4, s = r & 15;
+        const int x = s & 3, y = s >> 2, z = UP ? 3 : 0;
+        int q = 0;
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk)
+            if (kk == k) q = halo_dir(UP, kk);
+        int slot = 0;
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk)
+            if (kk == k) slot = slot_of<TABLE>(halo_dir(UP, kk), x, y, z);
+        const long long at = (tile_begin + t) * TILE_VALUES + q * 64 + slot;
+        if (PACK) buf[i] = f[at];
+        else f[at] = buf[i];
+    }
+}
+
+}  // namespace
+}  // namespace tlbm
+
+extern "C" int tlbm_halo(void *d_f, int dtype, int table, int64_t tile_begin, int64_t tile_end,
+                         int up, int pack, void *d_buf, void *stream) {
+    if (tile_end < tile_begin || tile_begin < 0) {
+        set_error("tlbm_halo: bad tile range");
+        return TLBM_ERR_ARG;
+    }
+    const long long nt = tile_end - tile_begin;
+    if (nt == 0) return TLBM_OK;
+    return dispatch(dtype, 0, table, [&]<class T, int QU, int TB>() {
+        auto *f = static_cast<T *>(d_f);
+        auto *b = static_cast<T *>(d_buf);
+        cudaStream_t s = as_stream(stream);
+        unsigned g = grid_capped(nt * 80);
+        if (up && pack) halo_kernel<T, TB, 1, true><<<g, 256, 0, s>>>(f, tile_begin, nt, b);
+        else if (up) halo_kernel<T, TB, 1, false><<<g, 256, 0, s>>>(f, tile_begin, nt, b);
+        else if (pack) halo_kernel<T, TB, 0, true><<<g, 256, 0, s>>>(f, tile_begin, nt, b);
+        else halo_kernel<T, TB, 0, false><<<g, 256, 0, s>>>(f, tile_begin, nt, b);
+        return launch_check("halo_kernel");
+    });
+}

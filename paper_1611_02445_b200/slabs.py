@@ -1,0 +1,321 @@
+"""Multi-GPU z-slab decomposition over tile layers.
+
+One process per GPU.  The global geometry is cut along z into slabs of whole
+4-node tile layers, balanced by non-solid node count.  Every rank builds the
+local geometry ``[ghost layer | owned layers | ghost layer]`` (the ghost layers
+are copies of the neighbours' boundary layers; with a periodic z axis the
+first and last ranks are neighbours) and runs the ordinary device tiler and
+step on it.  Because the tile list is z-outermost (tiling.py:70-75), the owned
+tiles are one contiguous index range and each layer is a sub-range, so the
+step kernel is simply launched on tile ranges.
+
+Per step (copy p -> 1-p):
+  1. step the owned bottom and top tile layers          (boundary)
+  2. pack their outgoing z planes (80 values per tile: 5 directions x 16
+     nodes; csrc/fields.cu tlbm_halo)
+  3. exchange with the z neighbours (NCCL send/recv on NCCL's stream, or
+     device copies between virtual ranks on one GPU)
+  4. step the interior layers -- concurrently with 3
+  5. unpack into the ghost layers of copy 1-p, flip parity
+Ghost node *tags* never change, so they are part of the local geometry and
+the per-node link masks of owned nodes are exact; only f values move.
+
+The exchange moves 640 B (fp64) per boundary tile per direction of travel;
+results are bit-identical to the single-domain run (tests).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .geometry import Geometry
+from .solver import SimulationConfig, Solver
+
+TILE = 4
+
+
+@dataclass
+class SlabRange:
+    rank: int
+    z0: int                 # first owned node layer (global)
+    z1: int                 # one past the last owned node layer (global)
+    lower: int              # rank owning the layer below (-1: none)
+    upper: int              # rank owning the layer above (-1: none)
+
+
+class SlabPlan:
+    """Partition of the global z extent into per-rank tile-layer ranges."""
+
+    def __init__(self, geometry, world):
+        nx, ny, nz = geometry.shape
+        self.world = int(world)
+        self.dims = (nx, ny, nz)
+        self.periodic_z = bool(geometry.periodic[2])
+        ntz = -(-nz // TILE)
+        if self.world < 1 or self.world > ntz:
+            raise ValueError(f"cannot cut {ntz} tile layers into {world} slabs")
+        if self.periodic_z and self.world > 1 and nz % TILE:
+            raise ValueError("periodic z needs a multiple of 4 layers")
+        # non-solid node count per tile layer -> balanced contiguous cuts
+        ns = np.count_nonzero(geometry.types, axis=(0, 1))
+        pad = np.zeros(ntz * TILE, dtype=np.int64)
+        pad[:nz] = ns
+        per_layer = pad.reshape(ntz, TILE).sum(1)
+        self.layer_weight = per_layer
+        cum = np.concatenate([[0], np.cumsum(per_layer)])
+        total = cum[-1]
+        cuts = [0]
+        for r in range(1, self.world):
+            target = total * r / self.world
+            c = int(np.searchsorted(cum, target))
+            if c > 0 and abs(cum[c - 1] - target) <= abs(cum[min(c, ntz)] - target):
+                c -= 1                      # nearest prefix boundary to the target
+            c = min(max(c, cuts[-1] + 1), ntz - (self.world - r))
+            cuts.append(c)
+        cuts.append(ntz)
+        self.ranges = []
+        for r in range(self.world):
+            lower = r - 1 if r > 0 else (self.world - 1 if self.periodic_z and self.world > 1
+                                         else -1)
+            upper = r + 1 if r < self.world - 1 else (0 if self.periodic_z and self.world > 1
+                                                     else -1)
+            self.ranges.append(SlabRange(r, cuts[r] * TILE, min(cuts[r + 1] * TILE, nz),
+                                         lower, upper))
+
+    def local_types(self, types, rank):
+        """[ghost below | owned | ghost above] tags of one rank."""
+        r = self.ranges[rank]
+        nz = self.dims[2]
+        parts = []
+        if r.lower >= 0:
+            lo = r.z0 - TILE
+            parts.append(types[:, :, lo:r.z0] if lo >= 0 else types[:, :, nz - TILE:nz])
+        parts.append(types[:, :, r.z0:r.z1])
+        if r.upper >= 0:
+            hi = r.z1 + TILE
+            parts.append(types[:, :, r.z1:hi] if hi <= nz else types[:, :, 0:TILE])
+        return np.ascontiguousarray(np.concatenate(parts, axis=2))
+
+    def local_geometry(self, geometry, rank):
+        per = tuple(geometry.periodic)
+        if self.world > 1:
+            per = (per[0], per[1], False)
+        return Geometry(self.local_types(geometry.types, rank), geometry.inlet_velocity,
+                        geometry.outlet_density, periodic=per)
+
+
+def layer_tile_ranges(tile_map):
+    """[begin, end) tile-index range of every local tile layer (tz)."""
+    occ = (tile_map >= 0).sum(axis=(0, 1)) if isinstance(tile_map, np.ndarray) else \
+        (tile_map >= 0).sum(dim=(0, 1)).cpu().numpy()
+    ends = np.cumsum(occ)
+    begins = ends - occ
+    return [(int(b), int(e)) for b, e in zip(begins, ends)]
+
+
+class SlabSolver:
+    """One rank's slab: a local Solver plus the halo bookkeeping."""
+
+    def __init__(self, geometry, plan, rank, config=None, device=None):
+        self.plan, self.rank = plan, rank
+        self.range = plan.ranges[rank]
+        self.local_geometry = plan.local_geometry(geometry, rank)
+        self.solver = Solver(self.local_geometry, config or SimulationConfig(), device)
+        s = self.solver
+        layers = layer_tile_ranges(s.tiling.tile_map)
+        has_lo, has_hi = self.range.lower >= 0, self.range.upper >= 0
+        own = layers[(1 if has_lo else 0):(len(layers) - 1 if has_hi else len(layers))]
+        self.ghost_lo = layers[0] if has_lo else None
+        self.ghost_hi = layers[-1] if has_hi else None
+        self.own = (own[0][0], own[-1][1])
+        self.bottom, self.top = own[0], own[-1]
+        self.interior = (self.bottom[1], self.top[0]) if len(own) > 2 else (self.top[0],
+                                                                            self.top[0])
+        self.n_fn_owned = int(s.tiling.counts[self.own[0]:self.own[1]].sum().item())
+        dt = s.store.tdtype
+        dev = s.device
+        nb = lambda r: torch.empty(max(r[1] - r[0], 0) * 80, dtype=dt, device=dev)  # noqa
+        self.send_up = nb(self.top) if has_hi else None
+        self.send_down = nb(self.bottom) if has_lo else None
+        self.recv_lo = nb(self.ghost_lo) if has_lo else None
+        self.recv_hi = nb(self.ghost_hi) if has_hi else None
+        if has_lo and self.recv_lo.numel() != (self.ghost_lo[1] - self.ghost_lo[0]) * 80:
+            raise AssertionError("ghost layer size mismatch")
+
+    # -- the pieces of one step ---------------------------------------------
+    def _launch(self, rng):
+        if rng[1] > rng[0]:
+            s = self.solver
+            a = s._args
+            a.tile_begin, a.tile_end = rng
+            a.f_src = s._copies[s.parity]
+            a.f_dst = s._copies[1 - s.parity]
+            a.flags = s.status.data_ptr() + 4 * (s.iteration % len(s.status))
+            nat.check(nat.load().tlbm_step(nat.ctypes.byref(a), nat.stream_ptr(s.device)))
+
+    def step_boundary(self):
+        self._launch(self.bottom)
+        if self.top != self.bottom:
+            self._launch(self.top)
+
+    def step_interior(self):
+        self._launch(self.interior)
+
+    def _halo(self, rng, up, pack, buf, copy):
+        s = self.solver
+        nat.call("tlbm_halo", nat.ptr(s.store.copy_tensor(copy)), s.code, s.table,
+                 rng[0], rng[1], int(up), int(pack), nat.ptr(buf), nat.stream_ptr(s.device))
+
+    def pack(self, current=False):
+        """Pack the outgoing planes of the copy just written (or, with
+        ``current``, of the current copy -- the initial ghost fill)."""
+        c = self.solver.parity if current else 1 - self.solver.parity
+        if self.send_up is not None:
+            self._halo(self.top, True, True, self.send_up, c)
+        if self.send_down is not None:
+            self._halo(self.bottom, False, True, self.send_down, c)
+
+    def unpack(self, current=False):
+        c = self.solver.parity if current else 1 - self.solver.parity
+        if self.recv_lo is not None:
+            self._halo(self.ghost_lo, True, False, self.recv_lo, c)
+        if self.recv_hi is not None:
+            self._halo(self.ghost_hi, False, False, self.recv_hi, c)
+
+    def finish(self):
+        s = self.solver
+        s.parity ^= 1
+        s.iteration += 1
+        if s.iteration - s._checked >= len(s.status) - 1:
+            s.check()
+
+    def fields_owned(self):
+        """Canonical (19, t_own, 64) of the owned tiles (current copy)."""
+        f = self.solver.fields_canonical(device=True)
+        return f[:, self.own[0]:self.own[1]]
+
+
+class NcclHalo:
+    """Neighbour exchange over torch.distributed (NCCL on GPUs).
+
+    Fixed post order on every rank -- sends [up, down], receives [from below,
+    from above] -- so that, with two ranks and periodic z, both messages to
+    the same peer match in order."""
+
+    def __init__(self, slab):
+        import torch.distributed as dist
+        self.dist, self.slab = dist, slab
+
+    def start(self):
+        d, sl, r = self.dist, self.slab, self.slab.range
+        ops = []
+        if sl.send_up is not None:
+            ops.append(d.P2POp(d.isend, sl.send_up, r.upper))
+        if sl.send_down is not None:
+            ops.append(d.P2POp(d.isend, sl.send_down, r.lower))
+        if sl.recv_lo is not None:
+            ops.append(d.P2POp(d.irecv, sl.recv_lo, r.lower))
+        if sl.recv_hi is not None:
+            ops.append(d.P2POp(d.irecv, sl.recv_hi, r.upper))
+        return d.batch_isend_irecv(ops) if ops else []
+
+    @staticmethod
+    def wait(reqs):
+        for q in reqs:
+            q.wait()
+
+
+class DistributedSlabRunner:
+    """Steps one rank of an N-GPU slab run; NCCL exchange overlapped with the
+    interior-tile launch."""
+
+    def __init__(self, geometry, world, rank, config=None, device=None):
+        self.plan = SlabPlan(geometry, world)
+        self.slab = SlabSolver(geometry, self.plan, rank, config, device)
+        self.halo = NcclHalo(self.slab) if world > 1 else None
+        self.n_fn_owned = self.slab.n_fn_owned
+
+    def exchange_current(self):
+        """Fill the ghost planes of the current copy from the neighbours (after
+        initialising each rank's fields independently)."""
+        if self.halo is None:
+            return
+        self.slab.pack(current=True)
+        NcclHalo.wait(self.halo.start())
+        self.slab.unpack(current=True)
+
+    def step(self, n=1):
+        sl = self.slab
+        for _ in range(int(n)):
+            if self.halo is None:
+                sl._launch(sl.own)
+                sl.finish()
+                continue
+            sl.step_boundary()
+            sl.pack()
+            reqs = self.halo.start()
+            sl.step_interior()
+            NcclHalo.wait(reqs)
+            sl.unpack()
+            sl.finish()
+
+    def barrier(self):
+        if self.halo is not None:
+            self.halo.dist.barrier()
+
+
+class VirtualSlabs:
+    """All slabs of a decomposition on ONE device, exchanged by device copies
+    -- exercises the partition, halo pack/unpack and ghost logic of the
+    multi-GPU path on a single GPU."""
+
+    def __init__(self, geometry, world, config=None, device=None):
+        self.plan = SlabPlan(geometry, world)
+        self.slabs = [SlabSolver(geometry, self.plan, r, config, device) for r in range(world)]
+
+    def _exchange(self):
+        for sl in self.slabs:
+            r = sl.range
+            if sl.send_up is not None:
+                self.slabs[r.upper].recv_lo.copy_(sl.send_up)
+            if sl.send_down is not None:
+                self.slabs[r.lower].recv_hi.copy_(sl.send_down)
+
+    def exchange_current(self):
+        for sl in self.slabs:
+            sl.pack(current=True)
+        self._exchange()
+        for sl in self.slabs:
+            sl.unpack(current=True)
+
+    def step(self, n=1):
+        for _ in range(int(n)):
+            for sl in self.slabs:
+                sl.step_boundary()
+                sl.pack()
+            self._exchange()
+            for sl in self.slabs:
+                sl.step_interior()
+                sl.unpack()
+                sl.finish()
+
+    def fields_owned(self):
+        return torch.cat([sl.fields_owned() for sl in self.slabs], dim=1)
+
+
+class SlabChannel(DistributedSlabRunner):
+    """Bench workload for N ranks: the 256^2 channel periodic along z,
+    256 * N long, one 256^3 slab per rank (weak scaling)."""
+
+    def __init__(self, n, world, rank, precision="f64", table="b200", device=None):
+        from . import workloads
+        geo = workloads.channel_z(n, n * world)
+        cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table)
+        super().__init__(geo, world, rank, cfg, device)
+        s = self.slab.solver
+        rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.04),
+                                            seed=1234 + rank)
+        s.init_from_macroscopic(rho, u)
+        self.exchange_current()

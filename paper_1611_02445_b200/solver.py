@@ -157,6 +157,7 @@ class Solver:
         nat.require_cuda(self.device)
         a = self._args
         a.variant = int(variant)
+        a.tile_begin, a.tile_end = 0, self.t_n
         stream = nat.stream_ptr(self.device)
         lib = nat.load()
         base = self.status.data_ptr()

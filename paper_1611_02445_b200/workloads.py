@@ -30,6 +30,13 @@ def channel(n=256, length=None):
                                      ends="periodic")
 
 
+def channel_z(n=256, length=None):
+    """The config-2 channel with its axis along z (the slab axis): n x n
+    cross-section, periodic in z, ``length`` nodes long (default n)."""
+    return geometry.generate_channel("square", n, axis=2, length=n if length is None else length,
+                                     ends="periodic")
+
+
 def sphere_pack(porosity, n=256, diameter=40, seed=1234):
     if porosity >= 1.0:
         return geometry.generate_box(n, flow_axis=2, inlet_velocity=(0.0, 0.0, 0.01))
