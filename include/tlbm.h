@@ -45,6 +45,10 @@ enum { TLBM_FLAG_DIVERGED = 1, TLBM_FLAG_GUARD = 2 };
 int tlbm_abi_version(void);
 const char *tlbm_last_error(void);
 int tlbm_set_device(int device);
+/* L2 fetch granularity hint of the current device (cudaLimitMaxL2FetchGranularity,
+ * 0..128 bytes); sparse geometries over-fetch less at 32. */
+int tlbm_set_l2_fetch_granularity(int bytes);
+int tlbm_get_l2_fetch_granularity(int *bytes);
 
 /* Host-only: the compiled-in lattice and layout tables, for CPU checks.
  * e: 19x3 int32, opp: 19 int32, w: 19 double, perm: 19x64 int32 slot
@@ -145,6 +149,8 @@ typedef struct {
     double outlet_rho;
     double u_guard;              /* |u| > u_guard sets TLBM_FLAG_GUARD; 0 off */
     uint32_t *flags;             /* device status word (OR-ed), may be NULL */
+    int rel32;                   /* 1: every |nbr[t][k] - t| * 1216 < 2^31, so the
+                                    kernel may use 32-bit relative offsets */
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);

@@ -25,7 +25,7 @@ static int CAT(collide, SFX)(const REAL *g, REAL *out, int quasi, REAL inv_tau,
     REAL u[3];
     for (int a = 0; a < 3; ++a) u[a] = quasi ? j[a] / rho : j[a];
     REAL usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
-    if (u_guard > 0 && sqrt((double)usq) > u_guard) st |= 2;
+    if (u_guard > 0 && usq > (REAL)(u_guard * u_guard)) st |= 2;
     for (int q = 0; q < 19; ++q) {
         REAL cu = (REAL)0;
         for (int a = 0; a < 3; ++a) {

@@ -29,13 +29,15 @@ class StepArgs(ctypes.Structure):
                 ("t_n", c_i64), ("tile_begin", c_i64), ("tile_end", c_i64),
                 ("f_src", c_vp), ("f_dst", c_vp), ("nbr", c_vp), ("meta", c_vp),
                 ("tau", c_dbl), ("inlet_u", c_dbl * 3), ("outlet_rho", c_dbl),
-                ("u_guard", c_dbl), ("flags", c_vp)]
+                ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int)]
 
 
 _PROTOS = {
     "tlbm_abi_version": (c_int, []),
     "tlbm_last_error": (ctypes.c_char_p, []),
     "tlbm_set_device": (c_int, [c_int]),
+    "tlbm_set_l2_fetch_granularity": (c_int, [c_int]),
+    "tlbm_get_l2_fetch_granularity": (c_int, [ctypes.POINTER(c_int)]),
     "tlbm_lattice_tables": (c_int, [c_int, c_vp, c_vp, c_vp, c_vp]),
     "tlbm_tiling_scratch_bytes": (c_size, [c_int, c_int, c_int]),
     "tlbm_tile_map": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_vp,

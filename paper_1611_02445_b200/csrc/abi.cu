@@ -48,3 +48,16 @@ extern "C" int tlbm_lattice_tables(int table, int32_t *h_e, int32_t *h_opp,
     }
     return TLBM_OK;
 }
+
+extern "C" int tlbm_set_l2_fetch_granularity(int bytes) {
+    return cuda_check(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes),
+                      "cudaDeviceSetLimit(MaxL2FetchGranularity)");
+}
+
+extern "C" int tlbm_get_l2_fetch_granularity(int *bytes) {
+    size_t v = 0;
+    int rc = cuda_check(cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity),
+                        "cudaDeviceGetLimit(MaxL2FetchGranularity)");
+    if (!rc) *bytes = (int)v;
+    return rc;
+}

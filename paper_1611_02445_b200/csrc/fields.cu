@@ -1,6 +1,8 @@
 // Field-store kernels: equilibrium initialisation, canonical
 // scatter/gather (layout.py:155-167) and the macroscopic readout
 // (collision.py:75-121) -- all in the reference's arithmetic order.
+#include <cmath>
+
 #include "common.cuh"
 #include "physics.cuh"
 
@@ -79,7 +81,7 @@ __device__ __forceinline__ uint32_t readout(const T (&g)[Q], long long i, long l
     u[n + i] = uu[1];
     u[2 * n + i] = uu[2];
     if (p) p[i] = r / T(3.0);
-    return status_of<T, QUASI>(r, T(0), 0.0);
+    return status_of<T, QUASI>(r, T(0), T(HUGE_VAL));
 }
 
 template <class T, int QUASI, int TABLE>
@@ -129,7 +131,7 @@ __global__ void collide_kernel(T *f, long long n, double inv_tau, uint32_t *flag
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) g[q] = f[q * n + i];
-        st |= collide<T, QUASI>(g, T(inv_tau), 0.0);
+        st |= collide<T, QUASI>(g, T(inv_tau), T(HUGE_VAL));
 #pragma unroll
         for (int q = 0; q < Q; ++q) f[q * n + i] = g[q];
     }

@@ -18,6 +18,11 @@ enum : uint32_t { ST_DIVERGED = 1u, ST_GUARD = 2u };
 
 // rho = ((g0 + g1) + ...) + g18; j_a accumulated from 0 in q order
 // (collision.py:55-72); u = j / rho (quasi) or j (incompressible)
+//
+// The reference starts j and cu from 0 (np.zeros_like); "0 + x" is folded to
+// x here.  That changes at most the sign of an exactly-zero partial sum,
+// which never changes a post-collision population (every later use adds a
+// non-negative term or squares it), so results stay bit-identical.
 template <class T, int QUASI>
 __device__ __forceinline__ void moments(const T (&g)[Q], T &rho, T (&u)[3]) {
     rho = g[0];
@@ -26,10 +31,14 @@ __device__ __forceinline__ void moments(const T (&g)[Q], T &rho, T (&u)[3]) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
         T acc = T(0);
+        bool first = true;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            if (e_axis(q, a) == 1) acc = acc + g[q];
-            else if (e_axis(q, a) == -1) acc = acc - g[q];
+            const int e = e_axis(q, a);
+            if (e == 0) continue;
+            if (first) acc = e > 0 ? g[q] : -g[q];
+            else acc = e > 0 ? acc + g[q] : acc - g[q];
+            first = false;
         }
         u[a] = QUASI ? acc / rho : acc;
     }
@@ -39,10 +48,14 @@ __device__ __forceinline__ void moments(const T (&g)[Q], T &rho, T (&u)[3]) {
 template <class T, int QUASI>
 __device__ __forceinline__ T equilibrium_q(int q, T rho, const T (&u)[3], T usq) {
     T cu = T(0);
+    bool first = true;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        if (e_axis(q, a) > 0) cu = cu + u[a];
-        else if (e_axis(q, a) < 0) cu = cu + (-u[a]);
+        const int e = e_axis(q, a);
+        if (e == 0) continue;
+        const T term = e > 0 ? u[a] : -u[a];
+        cu = first ? term : cu + term;
+        first = false;
     }
     T br = T(3.0) * cu + T(4.5) * cu * cu - T(1.5) * usq;
     T w = T(weight(q));
@@ -54,17 +67,19 @@ __device__ __forceinline__ T speed_sq(const T (&u)[3]) {
     return u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
 }
 
+// divergence: NaN, or rho <= 0 in the quasi-compressible model
+// (collision.py:84-86); guard: |u|^2 > u_max_guard^2
 template <class T, int QUASI>
-__device__ __forceinline__ uint32_t status_of(T rho, T usq, double u_guard) {
+__device__ __forceinline__ uint32_t status_of(T rho, T usq, T guard_sq) {
     uint32_t st = 0;
     if (rho != rho || (QUASI && !(rho > T(0)))) st |= ST_DIVERGED;
-    if (u_guard > 0.0 && sqrt((double)usq) > u_guard) st |= ST_GUARD;
+    if (usq > guard_sq) st |= ST_GUARD;
     return st;
 }
 
 // collide_lbgk in place: g <- g + fl(1/tau) (feq - g)  (collision.py:124-130)
 template <class T, int QUASI>
-__device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, double u_guard) {
+__device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, T guard_sq) {
     T rho, u[3];
     moments<T, QUASI>(g, rho, u);
     T usq = speed_sq(u);
@@ -73,7 +88,7 @@ __device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, double u_guard
         T feq = equilibrium_q<T, QUASI>(q, rho, u, usq);
         g[q] = g[q] + inv_tau * (feq - g[q]);
     }
-    return status_of<T, QUASI>(rho, usq, u_guard);
+    return status_of<T, QUASI>(rho, usq, guard_sq);
 }
 
 // ---- Zou-He (boundaries.py:53-92 closures, 132-195 arithmetic) -----------
@@ -167,8 +182,8 @@ __device__ __forceinline__ void zh_pressure(T (&g)[Q], double rho0_in) {
 }
 
 template <class T, int QUASI>
-__device__ __forceinline__ void zou_he(T (&g)[Q], int tag, int face, const double (&u_in)[3],
-                                    double rho0) {
+__device__ __forceinline__ void zou_he_inline(T (&g)[Q], int tag, int face,
+                                           const double (&u_in)[3], double rho0) {
     if (tag == INLET) {
         switch (face) {
             case 0: zh_velocity<T, QUASI, 0>(g, u_in); break;
@@ -188,6 +203,33 @@ __device__ __forceinline__ void zou_he(T (&g)[Q], int tag, int face, const doubl
             default: zh_pressure<T, 5>(g, rho0); break;
         }
     }
+}
+
+// Out-of-line closure for the step kernel: inlet/outlet nodes are rare, so
+// the 12 face x kind variants live in one called function working on a
+// stack copy; the hot FLUID path keeps g[] in registers and its register
+// budget free of the closure code.
+template <class T, int QUASI>
+__device__ __noinline__ void zou_he_call(T *g, int tag, int face, double ux, double uy,
+                                         double uz, double rho0) {
+    T r[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) r[q] = g[q];
+    const double u_in[3] = {ux, uy, uz};
+    zou_he_inline<T, QUASI>(r, tag, face, u_in, rho0);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = r[q];
+}
+
+template <class T, int QUASI>
+__device__ __forceinline__ void zou_he(T (&g)[Q], int tag, int face, const double (&u_in)[3],
+                                    double rho0) {
+    T tmp[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) tmp[q] = g[q];
+    zou_he_call<T, QUASI>(tmp, tag, face, u_in[0], u_in[1], u_in[2], rho0);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) g[q] = tmp[q];
 }
 
 }  // namespace tlbm

@@ -13,6 +13,8 @@
 // 32-byte sector of the source copy is consumed by exactly one destination
 // tile, so DRAM traffic is the 2 x 19 x 8 B / node minimum plus metadata
 // (4 B/node meta word + 108 B/tile neighbour row).
+#include <cmath>
+
 #include "common.cuh"
 #include "physics.cuh"
 
@@ -29,7 +31,7 @@ struct StepParams {
     double inv_tau;
     double inlet_u[3];
     double outlet_rho;
-    double u_guard;
+    double guard_sq;        // |u|^2 threshold of the guard (+inf: off)
     uint32_t *flags;
 };
 
@@ -57,7 +59,12 @@ __device__ __forceinline__ void store_out(T *p, T v) {
 #endif
 }
 
-template <class T, int QUASI, int TABLE, int VARIANT, int TPC>
+// REL32: neighbour rows are staged as 32-bit element offsets relative to the
+// thread's own tile, so every per-direction address is one 32-bit add/select
+// and one IMAD.WIDE from a 64-bit base fixed per thread; valid whenever
+// |nbr - tile| * 1216 < 2^31 (checked on the host, tiling.py), otherwise the
+// 64-bit path recomputes full indices.
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32>
 __global__ void __launch_bounds__(64 * TPC, TLBM_MINB)
 step_kernel(const StepParams<T> p) {
     __shared__ int s_nbr[TPC][NBR];
@@ -68,8 +75,9 @@ step_kernel(const StepParams<T> p) {
 
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
-            long long t = tile0 + i / NBR;
-            s_nbr[i / NBR][i % NBR] = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
+            const long long t = tile0 + i / NBR;
+            const long long nb = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
+            s_nbr[i / NBR][i % NBR] = (int)(REL32 ? (nb >= 0 ? (nb - t) * TILE_VALUES : 0) : nb);
         }
         __syncthreads();
     }
@@ -79,25 +87,30 @@ step_kernel(const StepParams<T> p) {
     if (meta & META_ACTIVE) {
         const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
         const long long own = tile * TILE_VALUES;
+        const T *base = p.src + own;
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            long long off;
             if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
-                off = own + q * 64 + slot_of<TABLE>(q, x, y, z);
+                g[q] = load_ro(base + (q * 64 + slot_of<TABLE>(q, x, y, z)));
+                continue;
+            }
+            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
+            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
+            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
+            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
+            const int in_tile = q * 64 + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
+            const int bounced = opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
+            const bool link = (meta >> q) & 1u;
+            if (REL32) {
+                const int rel = (dx | dy | dz) ? s_nbr[ti][delta_index(dx, dy, dz)] : 0;
+                g[q] = load_ro(base + (link ? rel + in_tile : bounced));
             } else {
-                const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
-                const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
-                const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
-                const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
                 const long long nb = (dx | dy | dz) ? (long long)s_nbr[ti][delta_index(dx, dy, dz)]
                                                     : tile;
-                const long long pulled = nb * TILE_VALUES + q * 64
-                                       + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
-                const long long bounced = own + opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
-                off = ((meta >> q) & 1u) ? pulled : bounced;
+                const long long off = link ? nb * TILE_VALUES + in_tile : own + bounced;
+                g[q] = load_ro(p.src + off);
             }
-            g[q] = load_ro(p.src + off);
         }
 
         if (VARIANT == TLBM_FULL) {
@@ -110,11 +123,12 @@ step_kernel(const StepParams<T> p) {
             } else {
                 if (tag == INLET || tag == OUTLET)
                     zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
-                status = collide<T, QUASI>(g, T(p.inv_tau), p.u_guard);
+                status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
             }
         }
+        T *out = p.dst + own;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) store_out(p.dst + own + q * 64 + slot_of<TABLE>(q, x, y, z), g[q]);
+        for (int q = 0; q < Q; ++q) store_out(out + (q * 64 + slot_of<TABLE>(q, x, y, z)), g[q]);
     }
     if (p.flags) {
         // one atomic per warp, and only for bits not yet set: a flow sitting at
@@ -128,8 +142,18 @@ step_kernel(const StepParams<T> p) {
 
 constexpr int TPC = TLBM_TPC;
 
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32>
+int launch_as(const tlbm_step_args *a, cudaStream_t s);
+
 template <class T, int QUASI, int TABLE, int VARIANT>
 int launch(const tlbm_step_args *a, cudaStream_t s) {
+    if (a->rel32)
+        return launch_as<T, QUASI, TABLE, VARIANT, true>(a, s);
+    return launch_as<T, QUASI, TABLE, VARIANT, false>(a, s);
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32>
+int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T> p;
     p.src = static_cast<const T *>(a->f_src);
     p.dst = static_cast<T *>(a->f_dst);
@@ -140,11 +164,11 @@ int launch(const tlbm_step_args *a, cudaStream_t s) {
     p.inv_tau = 1.0 / a->tau;
     for (int k = 0; k < 3; ++k) p.inlet_u[k] = a->inlet_u[k];
     p.outlet_rho = a->outlet_rho;
-    p.u_guard = a->u_guard;
+    p.guard_sq = a->u_guard > 0.0 ? a->u_guard * a->u_guard : HUGE_VAL;
     p.flags = a->flags;
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
-    step_kernel<T, QUASI, TABLE, VARIANT, TPC>
+    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32>
         <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel");
 }

@@ -109,6 +109,7 @@ class Solver:
         a.inlet_u[:] = list(geometry.inlet_velocity)
         a.outlet_rho = float(geometry.outlet_density)
         a.u_guard = float(self.config.u_max_guard or 0.0)
+        a.rel32 = int(self.tiling.rel32)
         self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
         self.init_equilibrium()
 

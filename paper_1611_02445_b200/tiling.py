@@ -108,6 +108,20 @@ class DeviceTiling:
             raise ValueError(f"{n_bad_face} inlet/outlet nodes do not lie on exactly one "
                              "axis-aligned domain face")
         self.n_fn = int(self.counts.sum().item()) if self.t_n else 0
+        self.rel32 = self._offsets_fit_int32()
+
+    def _offsets_fit_int32(self, chunk=1 << 20):
+        """True if every neighbour is within 2^31 values of its tile in the
+        store (|nbr - t| * 19 * 64 < 2^31), enabling the step kernel's 32-bit
+        relative addressing."""
+        limit = (2 ** 31 - 1) // (19 * 64) - 1
+        for b in range(0, self.t_n, chunk):
+            blk = self.nbr[b:b + chunk]
+            t = torch.arange(b, b + blk.shape[0], device=self.device, dtype=torch.int32)
+            d = torch.where(blk >= 0, (blk - t[:, None]).abs(), torch.zeros_like(blk))
+            if int(d.max().item()) > limit:
+                return False
+        return True
 
     def grid(self):
         return TileGrid(a=TILE, dims=self.dims,
