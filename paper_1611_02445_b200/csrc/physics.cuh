@@ -78,15 +78,47 @@ __device__ __forceinline__ uint32_t status_of(T rho, T usq, T guard_sq) {
 }
 
 // collide_lbgk in place: g <- g + fl(1/tau) (feq - g)  (collision.py:124-130)
+//
+// Opposite directions share their products: c.u of opp(q) is exactly -c.u of
+// q, so 3 cu and (4.5 cu) cu are computed once per pair and the reference's
+// bracket 3cu + 4.5cu*cu - 1.5usq becomes (A + B) - C for q and (B - A) - C
+// for opp(q) -- the same IEEE results ((-A) + B == B - A), fewer instructions.
+template <class T, int QUASI>
+__device__ __forceinline__ T feq_of(int q, T rho, T br) {
+    const T w = T(weight(q));
+    return QUASI ? w * (rho * (T(1.0) + br)) : w * (rho + br);
+}
+
 template <class T, int QUASI>
 __device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, T guard_sq) {
     T rho, u[3];
     moments<T, QUASI>(g, rho, u);
-    T usq = speed_sq(u);
+    const T usq = speed_sq(u);
+    const T c15 = T(1.5) * usq;
+    {
+        const T br = (T(3.0) * T(0) + T(4.5) * T(0) * T(0)) - c15;   // q = 0: cu = 0
+        g[0] = g[0] + inv_tau * (feq_of<T, QUASI>(0, rho, br) - g[0]);
+    }
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        T feq = equilibrium_q<T, QUASI>(q, rho, u, usq);
-        g[q] = g[q] + inv_tau * (feq - g[q]);
+    for (int q = 1; q < Q; ++q) {
+        if (opp(q) < q) continue;
+        const int o = opp(q);
+        T cu = T(0);
+        bool first = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int e = e_axis(q, a);
+            if (e == 0) continue;
+            const T term = e > 0 ? u[a] : -u[a];
+            cu = first ? term : cu + term;
+            first = false;
+        }
+        const T A = T(3.0) * cu;
+        const T B = T(4.5) * cu * cu;
+        const T fq = feq_of<T, QUASI>(q, rho, (A + B) - c15);
+        const T fo = feq_of<T, QUASI>(o, rho, (B - A) - c15);
+        g[q] = g[q] + inv_tau * (fq - g[q]);
+        g[o] = g[o] + inv_tau * (fo - g[o]);
     }
     return status_of<T, QUASI>(rho, usq, guard_sq);
 }

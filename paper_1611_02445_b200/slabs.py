@@ -227,14 +227,52 @@ class NcclHalo:
             q.wait()
 
 
+class HostStagedHalo(NcclHalo):
+    """The same exchange through host memory over a CPU process group (gloo):
+    lets several ranks share one GPU in tests of the multi-process path."""
+
+    def __init__(self, slab):
+        super().__init__(slab)
+        sl = slab
+        self.h_recv_lo = torch.empty(sl.recv_lo.shape, dtype=sl.recv_lo.dtype) \
+            if sl.recv_lo is not None else None
+        self.h_recv_hi = torch.empty(sl.recv_hi.shape, dtype=sl.recv_hi.dtype) \
+            if sl.recv_hi is not None else None
+
+    def start(self):
+        d, sl, r = self.dist, self.slab, self.slab.range
+        ops = []
+        if sl.send_up is not None:
+            ops.append(d.P2POp(d.isend, sl.send_up.cpu(), r.upper))
+        if sl.send_down is not None:
+            ops.append(d.P2POp(d.isend, sl.send_down.cpu(), r.lower))
+        if sl.recv_lo is not None:
+            ops.append(d.P2POp(d.irecv, self.h_recv_lo, r.lower))
+        if sl.recv_hi is not None:
+            ops.append(d.P2POp(d.irecv, self.h_recv_hi, r.upper))
+        return (d.batch_isend_irecv(ops) if ops else [], self)
+
+    @staticmethod
+    def wait(handle):
+        reqs, self = handle
+        for q in reqs:
+            q.wait()
+        if self.h_recv_lo is not None:
+            self.slab.recv_lo.copy_(self.h_recv_lo)
+        if self.h_recv_hi is not None:
+            self.slab.recv_hi.copy_(self.h_recv_hi)
+
+
 class DistributedSlabRunner:
     """Steps one rank of an N-GPU slab run; NCCL exchange overlapped with the
-    interior-tile launch."""
+    interior-tile launch.  ``transport="gloo"`` stages the halo through host
+    memory instead (tests with several ranks on one GPU)."""
 
-    def __init__(self, geometry, world, rank, config=None, device=None):
+    def __init__(self, geometry, world, rank, config=None, device=None, transport="nccl"):
         self.plan = SlabPlan(geometry, world)
         self.slab = SlabSolver(geometry, self.plan, rank, config, device)
-        self.halo = NcclHalo(self.slab) if world > 1 else None
+        halo_cls = HostStagedHalo if transport == "gloo" else NcclHalo
+        self.halo = halo_cls(self.slab) if world > 1 else None
         self.n_fn_owned = self.slab.n_fn_owned
 
     def exchange_current(self):
@@ -243,7 +281,7 @@ class DistributedSlabRunner:
         if self.halo is None:
             return
         self.slab.pack(current=True)
-        NcclHalo.wait(self.halo.start())
+        self.halo.wait(self.halo.start())
         self.slab.unpack(current=True)
 
     def step(self, n=1):
@@ -257,7 +295,7 @@ class DistributedSlabRunner:
             sl.pack()
             reqs = self.halo.start()
             sl.step_interior()
-            NcclHalo.wait(reqs)
+            self.halo.wait(reqs)
             sl.unpack()
             sl.finish()
 

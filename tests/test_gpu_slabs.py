@@ -95,3 +95,61 @@ def test_slab_channel_single_rank_runs():
     s = run.slab.solver
     s.check()
     assert run.n_fn_owned == 32 ** 3 and s.iteration == 5
+
+
+def _mp_worker(rank, world, port, steps, out):
+    import os
+
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    geo = CASES["pack_io"]()
+    cfg = solver.SimulationConfig(u_max_guard=0.0)
+    run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport="gloo")
+    s = run.slab.solver
+    f0 = _f0(geo, np.float64)
+    fl = _local_f(f0, run.slab.range, geo.shape[2])
+    s.set_fields_canonical(dense.to_canonical(fl, s.tile_grid.non_empty, np.zeros(19)))
+    run.step(steps)
+    d = s.to_dense(s.fields_canonical(device=True))
+    lo = TILE if run.slab.range.lower >= 0 else 0
+    r = run.slab.range
+    out[rank] = (r.z0, r.z1, d[..., lo:lo + r.z1 - r.z0].cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multiprocess_runner_gloo_on_one_gpu(world):
+    """DistributedSlabRunner in `world` processes sharing cuda:0 (halo staged
+    through host memory over gloo) == the single-domain step."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    steps = 10
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, steps, out))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    geo = CASES["pack_io"]()
+    cfg = solver.SimulationConfig(u_max_guard=0.0)
+    ref = solver.Solver(geo, cfg)
+    ref.set_fields_canonical(dense.to_canonical(_f0(geo, np.float64), ref.tile_grid.non_empty,
+                                                np.zeros(19)))
+    ref.step(steps)
+    want = ref.to_dense(ref.fields_canonical(device=True)).cpu().numpy()
+    got = np.zeros_like(want)
+    for rank in range(world):
+        z0, z1, d = out[rank]
+        got[..., z0:z1] = d
+    mask = geo.types != 0
+    assert np.array_equal(got[:, mask], want[:, mask])
