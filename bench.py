@@ -52,11 +52,14 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--precision", default="f64", choices=["f64", "f32"])
-    p.add_argument("--n", type=int, default=256, help="channel edge (nodes)")
+    p.add_argument("--edge", type=int, default=256, help="channel edge in nodes")
     p.add_argument("--table", default="b200")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--transport", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo stages halos through host memory (tests: several ranks "
+                        "may share one GPU); numbers are not representative")
     return p.parse_args()
 
 
@@ -177,7 +180,7 @@ def run_reference(args):
     from paper_1611_02445_b200 import workloads
     dt = np.float64 if args.precision == "f64" else np.float32
     length = 32
-    geo = workloads.channel_z(args.n, length=length)
+    geo = workloads.channel_z(args.edge, length=length)
     f0 = dense.init_equilibrium(geo.shape, "incompressible", dt, 1.0, (0.0, 0.0, 0.04))
     cores = len(os.sched_getaffinity(0))
     o = c_oracle.DenseOracle(geo.types, "incompressible", workloads.TAU, periodic=geo.periodic,
@@ -192,13 +195,13 @@ def run_reference(args):
     total = sum(t_all)
     value = n_fn * args.steps / total / 1e6
     sample = (f"C oracle port (oracle/tlbm_oracle.c, OpenMP x{cores}): each step = one full "
-              f"step of the channel {args.n}x{args.n}x{length} slab (periodic z), "
+              f"step of the channel {args.edge}x{args.edge}x{length} slab (periodic z), "
               f"{args.precision}; the reference has no step of its own (SURVEY 0.2)")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": f"channel{args.n}_periodic_{args.precision}",
+            "config": {"workload": f"channel{args.edge}_periodic_{args.precision}",
                        "sample_nodes": n_fn},
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -209,62 +212,76 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- GPU arm
-def workloads_tiles(geo):
-    """Non-empty tile count of a geometry (host-side sizing of the pinned
-    result buffers; the oracle tiler restatement is not needed -- a reshape)."""
-    t = geo.types
-    nx, ny, nz = t.shape
-    pad = np.zeros(tuple(-(-n // 4) * 4 for n in t.shape), dtype=bool)
-    pad[:nx, :ny, :nz] = t != 0
-    m = pad.reshape(pad.shape[0] // 4, 4, pad.shape[1] // 4, 4, pad.shape[2] // 4, 4)
-    return int(m.any(axis=(1, 3, 5)).sum())
-
-
-def e2e_run(args, torch, geo_host):
-    """Public API end to end from host data: Solver(geometry) [H2D of the
-    tags, device tiler + metadata, init], K x step() each with an async D2H of
-    that step's status word to pinned memory, final rho/u readout to pinned
-    host memory.  Phase times (host clock, a sync at each phase end) are
-    reported beside the total."""
+def e2e_run(args, torch, geo_host, world, rank, dist):
+    """Public API end to end from host data, on every rank:
+    DistributedSlabRunner(geometry) [slab cut, H2D of the local tags, device
+    tiler + metadata, init, initial ghost exchange], K x step() each followed
+    by an async D2H of that step's status word to pinned memory, and the final
+    rho/u readout of the owned tiles into pinned host buffers (allocated once,
+    outside the timed region, like the status buffer).  Time = max over ranks;
+    phase times (host clock, a sync at each phase end) reported beside it."""
+    from paper_1611_02445_b200 import slabs
     from paper_1611_02445_b200 import solver as sv
     cfg = sv.SimulationConfig(tau=0.6, precision=args.precision, table=args.table)
-    pinned = torch.empty(args.steps, dtype=torch.int32, pin_memory=True)
     dt = torch.float64 if args.precision == "f64" else torch.float32
-    # host result buffers are pinned once, outside the timed region (like the
-    # status ring); the readout copies into them
-    t_n = workloads_tiles(geo_host)
-    rho = torch.empty((t_n, 64), dtype=dt, pin_memory=True)
-    u = torch.empty((3, t_n, 64), dtype=dt, pin_memory=True)
+    plan = slabs.SlabPlan(geo_host, world)
+    r = plan.ranges[rank]
+    t_own = _tiles_in(geo_host.types[:, :, r.z0:r.z1])
+    pinned = torch.empty(args.steps, dtype=torch.int32, pin_memory=True)
+    rho = torch.empty((t_own, 64), dtype=dt, pin_memory=True)
+    u = torch.empty((3, t_own, 64), dtype=dt, pin_memory=True)
+    if dist is not None:
+        dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = sv.Solver(geo_host, cfg)
+    run = slabs.DistributedSlabRunner(geo_host, world, rank, cfg, transport=args.transport)
+    s = run.slab.solver
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04))
+    run.exchange_current()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     for i in range(args.steps):
-        s.step(1, check=False)
+        run.step(1)
         slot = (s.iteration - 1) % sv.STATUS_RING
         pinned[i:i + 1].copy_(s.status[slot:slot + 1], non_blocking=True)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     rho_d, u_d, _ = s.macroscopic(device=True)
-    rho.copy_(rho_d, non_blocking=True)
-    u.copy_(u_d, non_blocking=True)
+    b, e = run.slab.own
+    rho.copy_(rho_d[b:e], non_blocking=True)
+    u.copy_(u_d[:, b:e], non_blocking=True)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     el = t3 - t0
-    phases = {"setup_s": t1 - t0, "steps_s": t2 - t1, "readout_s": t3 - t2}
     if np.any(pinned.numpy() & 1):
         raise RuntimeError("e2e run diverged")
-    h2d = geo_host.types.nbytes
+    n_fn = run.n_fn_owned
+    h2d = run.slab.local_geometry.types.nbytes
     d2h = 4 * args.steps + rho.numel() * rho.element_size() + u.numel() * u.element_size()
-    n_fn = s.n_fn
-    del s, rho_d, u_d
+    if dist is not None:
+        v = torch.tensor([el, n_fn, h2d, d2h], dtype=torch.float64,
+                         device="cuda" if args.transport == "nccl" else "cpu")
+        mx = v.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v)
+        el, n_fn, h2d, d2h = float(mx[0]), int(v[1]), float(v[2]), float(v[3])
+    del run, s, rho_d, u_d
     return {"value": n_fn * args.steps / el / 1e6, "unit": UNIT,
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-            "seconds": el, "phases": phases,
-            "what": "Solver(geometry) + init + K x step() with per-step async D2H of the "
-                    "status word + final rho/u readout to pinned host memory"}
+            "seconds": el,
+            "phases": {"setup_s": t1 - t0, "steps_s": t2 - t1, "readout_s": t3 - t2},
+            "what": "DistributedSlabRunner(geometry) + init + K x step() with per-step async "
+                    "D2H of the status word + final owned rho/u readout to pinned host "
+                    "memory; max over ranks"}
+
+
+def _tiles_in(types):
+    """Non-empty 4^3 tiles of a voxel block (sizes the pinned result buffers)."""
+    nx, ny, nz = types.shape
+    pad = np.zeros(tuple(-(-n // 4) * 4 for n in types.shape), dtype=bool)
+    pad[:nx, :ny, :nz] = types != 0
+    m = pad.reshape(pad.shape[0] // 4, 4, pad.shape[1] // 4, 4, pad.shape[2] // 4, 4)
+    return int(m.any(axis=(1, 3, 5)).sum())
 
 
 def run_b200(args):
@@ -273,13 +290,19 @@ def run_b200(args):
     from paper_1611_02445_b200 import txmodel, workloads
 
     rank, world, local = dist_env()
+    if args.transport == "gloo" and torch.cuda.device_count() < world:
+        local = 0                    # test mode: ranks share one GPU
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.transport == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     from paper_1611_02445_b200 import slabs
-    runner = slabs.SlabChannel(args.n, world, rank, precision=args.precision, table=args.table)
+    runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision, table=args.table,
+                               transport=args.transport)
     n_fn_rank = runner.n_fn_owned
     step_fn = runner.step
     sync_all = runner.barrier
@@ -301,10 +324,11 @@ def run_b200(args):
         sync_all()
     ms = start.elapsed_time(end)
     if dist is not None:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        red_dev = "cuda" if args.transport == "nccl" else "cpu"
+        t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        nf = torch.tensor([n_fn_rank], device="cuda", dtype=torch.float64)
+        nf = torch.tensor([n_fn_rank], device=red_dev, dtype=torch.float64)
         dist.all_reduce(nf)
         n_fn_total = int(nf.item())
     else:
@@ -319,17 +343,17 @@ def run_b200(args):
     alg_bytes = n_fn_rank * b_node
     achieved = alg_bytes / (ms_step / 1e3) / 1e9
     peak, peak_src = peaks()
-    key = f"channel{args.n}_{args.precision}_{args.table}"
+    key = f"channel{args.edge}_{args.precision}_{args.table}"
     traffic = traffic_from_profiles(key)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-        "config": {"workload": f"channel{args.n}_periodic_{args.precision}"
+        "config": {"workload": f"channel{args.edge}_periodic_{args.precision}"
                                + (f"_slab_x{world}" if world > 1 else ""),
-                   "geometry": f"square channel d={args.n} along z, BB ring, periodic z, "
-                               f"{args.n}x{args.n}x{args.n} per GPU"
-                               + (f", global {args.n}x{args.n}x{args.n * world}"
+                   "geometry": f"square channel d={args.edge} along z, BB ring, periodic z, "
+                               f"{args.edge}x{args.edge}x{args.edge} per GPU"
+                               + (f", global {args.edge}x{args.edge}x{args.edge * world}"
                                   if world > 1 else ""),
                    "model": "LBGK incompressible, tau=0.6", "layout_table": args.table,
                    "n_fn_per_gpu": n_fn_rank, "t_n_per_gpu": n_fn_rank // 64,
@@ -343,14 +367,15 @@ def run_b200(args):
                      "metadata_bytes_per_launch": txmodel.metadata_bytes(n_fn_rank // 64),
                      "peak_source": peak_src, "frac_of_8TBs_spec": achieved / 8000.0},
         "clocks": clocks.report(),
-        "gpu_launches": args.steps,
+        "gpu_launches": args.steps * runner.launches_per_step(),
     }
-    if rank == 0 and world == 1 and not args.no_e2e:
+    if not args.edgeo_e2e:
         del runner
         torch.cuda.empty_cache()
-        line["e2e"] = e2e_run(args, torch, workloads.channel_z(args.n))
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_oracle_mlups(args.precision, args.n, args.cpu_seconds)
+        line["e2e"] = e2e_run(args, torch, workloads.channel_z(args.edge, args.edge * world), world,
+                              rank, dist)
+    if rank == 0 and world == 1 and not args.edgeo_cpu:
+        line["cpu_baseline"] = cpu_oracle_mlups(args.precision, args.edge, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -58,6 +58,10 @@ class SlabPlan:
             raise ValueError(f"cannot cut {ntz} tile layers into {world} slabs")
         if self.periodic_z and self.world > 1 and nz % TILE:
             raise ValueError("periodic z needs a multiple of 4 layers")
+        if self.world == 1:
+            self.layer_weight = None
+            self.ranges = [SlabRange(0, 0, nz, -1, -1)]
+            return
         # non-solid node count per tile layer -> balanced contiguous cuts
         ns = np.count_nonzero(geometry.types, axis=(0, 1))
         pad = np.zeros(ntz * TILE, dtype=np.int64)
@@ -99,6 +103,8 @@ class SlabPlan:
         return np.ascontiguousarray(np.concatenate(parts, axis=2))
 
     def local_geometry(self, geometry, rank):
+        if self.world == 1:
+            return geometry
         per = tuple(geometry.periodic)
         if self.world > 1:
             per = (per[0], per[1], False)
@@ -275,6 +281,16 @@ class DistributedSlabRunner:
         self.halo = halo_cls(self.slab) if world > 1 else None
         self.n_fn_owned = self.slab.n_fn_owned
 
+    def launches_per_step(self):
+        """Kernels of this library launched per step (step ranges + halo)."""
+        sl = self.slab
+        if self.halo is None:
+            return 1
+        n = 1 if sl.top == sl.bottom else 2
+        n += int(sl.interior[1] > sl.interior[0])
+        n += sum(b is not None for b in (sl.send_up, sl.send_down, sl.recv_lo, sl.recv_hi))
+        return n
+
     def exchange_current(self):
         """Fill the ghost planes of the current copy from the neighbours (after
         initialising each rank's fields independently)."""
@@ -347,11 +363,12 @@ class SlabChannel(DistributedSlabRunner):
     """Bench workload for N ranks: the 256^2 channel periodic along z,
     256 * N long, one 256^3 slab per rank (weak scaling)."""
 
-    def __init__(self, n, world, rank, precision="f64", table="b200", device=None):
+    def __init__(self, n, world, rank, precision="f64", table="b200", device=None,
+                 transport="nccl"):
         from . import workloads
         geo = workloads.channel_z(n, n * world)
         cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table)
-        super().__init__(geo, world, rank, cfg, device)
+        super().__init__(geo, world, rank, cfg, device, transport)
         s = self.slab.solver
         rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.04),
                                             seed=1234 + rank)

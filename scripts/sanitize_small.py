@@ -1,0 +1,26 @@
+"""Small runs of every kernel family for compute-sanitizer (memcheck /
+racecheck / initcheck) on the GPU box."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1611_02445_b200 import _native as nat  # noqa: E402
+from paper_1611_02445_b200 import collision, geometry, slabs, solver  # noqa: E402
+
+geo = geometry.generate_sphere_pack(20, 6, 0.6, seed=3, inlet_velocity=(0, 0, 0.02))
+for prec in ("f64", "f32"):
+    for fluid in ("incompressible", "quasi-compressible"):
+        s = solver.Solver(geo, solver.SimulationConfig(precision=prec, fluid=fluid))
+        s.step(3)
+        s.step(1, variant=nat.PROPAGATION_ONLY)
+        s.step(1, variant=nat.READ_WRITE_ONLY)
+        s.macroscopic()
+        s.fields_canonical()
+vs = slabs.VirtualSlabs(geometry.generate_channel("square", 12, axis=2, length=24,
+                                                  ends="periodic"), 3)
+vs.step(3)
+f = np.random.default_rng(0).random((19, 10))
+collision.collide_lbgk("incompressible", f, 0.7)
+print("sanitize run ok")
