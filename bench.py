@@ -369,12 +369,12 @@ def run_b200(args):
         "clocks": clocks.report(),
         "gpu_launches": args.steps * runner.launches_per_step(),
     }
-    if not args.edgeo_e2e:
+    if not args.no_e2e:
         del runner
         torch.cuda.empty_cache()
         line["e2e"] = e2e_run(args, torch, workloads.channel_z(args.edge, args.edge * world), world,
                               rank, dist)
-    if rank == 0 and world == 1 and not args.edgeo_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_oracle_mlups(args.precision, args.edge, args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
