@@ -57,9 +57,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    p.add_argument("--transport", default="nccl", choices=["nccl", "gloo"],
-                   help="gloo stages halos through host memory (tests: several ranks "
-                        "may share one GPU); numbers are not representative")
+    p.add_argument("--transport", default="ipc", choices=["ipc", "nccl", "gloo"],
+                   help="N>1 halo: ipc = fused peer stores from the step kernel (default), "
+                        "nccl = pack + NCCL send/recv + unpack, gloo = host-staged (tests)")
     return p.parse_args()
 
 
@@ -234,7 +234,8 @@ def e2e_run(args, torch, geo_host, world, rank, dist):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    run = slabs.DistributedSlabRunner(geo_host, world, rank, cfg, transport=args.transport)
+    run = slabs.DistributedSlabRunner(geo_host, world, rank, cfg,
+                                      transport=getattr(args, "transport_used", args.transport))
     s = run.slab.solver
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04))
     run.exchange_current()
@@ -256,11 +257,14 @@ def e2e_run(args, torch, geo_host, world, rank, dist):
     if np.any(pinned.numpy() & 1):
         raise RuntimeError("e2e run diverged")
     n_fn = run.n_fn_owned
+    if run.ipc is not None:
+        run.ipc.check()
+        run.ipc.close()
     h2d = run.slab.local_geometry.types.nbytes
     d2h = 4 * args.steps + rho.numel() * rho.element_size() + u.numel() * u.element_size()
     if dist is not None:
         v = torch.tensor([el, n_fn, h2d, d2h], dtype=torch.float64,
-                         device="cuda" if args.transport == "nccl" else "cpu")
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
         mx = v.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(v)
@@ -290,19 +294,33 @@ def run_b200(args):
     from paper_1611_02445_b200 import txmodel, workloads
 
     rank, world, local = dist_env()
-    if args.transport == "gloo" and torch.cuda.device_count() < world:
-        local = 0                    # test mode: ranks share one GPU
+    shared = torch.cuda.device_count() < world      # test mode: ranks share one GPU
+    if shared and args.transport == "nccl":
+        raise SystemExit("NCCL needs one GPU per rank; use --transport ipc|gloo to share one")
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
+    backend = "gloo" if (shared or args.transport == "gloo") else "nccl"
     if world > 1:
         import torch.distributed as dist
-        if args.transport == "nccl":
+        if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
     from paper_1611_02445_b200 import slabs
-    runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision, table=args.table,
-                               transport=args.transport)
+    transport = args.transport
+    try:
+        runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision,
+                                   table=args.table, transport=transport)
+    except RuntimeError as exc:
+        if transport != "ipc":
+            raise
+        print(f"[bench] ipc halo unavailable ({exc}); falling back to nccl", file=sys.stderr)
+        transport = "nccl" if backend == "nccl" else "gloo"
+        runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision,
+                                   table=args.table, transport=transport)
+    args.transport_used = transport
     n_fn_rank = runner.n_fn_owned
     step_fn = runner.step
     sync_all = runner.barrier
@@ -324,7 +342,7 @@ def run_b200(args):
         sync_all()
     ms = start.elapsed_time(end)
     if dist is not None:
-        red_dev = "cuda" if args.transport == "nccl" else "cpu"
+        red_dev = "cuda" if backend == "nccl" else "cpu"
         t = torch.tensor([ms], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -333,8 +351,10 @@ def run_b200(args):
         n_fn_total = int(nf.item())
     else:
         n_fn_total = n_fn_rank
-    # divergence check outside the timed region
+    # divergence / neighbour-timeout checks outside the timed region
     runner.slab.solver.check()
+    if runner.ipc is not None:
+        runner.ipc.check()
 
     ms_step = ms / args.steps
     value = n_fn_total * args.steps / (ms / 1e3) / 1e6
@@ -359,7 +379,9 @@ def run_b200(args):
                    "n_fn_per_gpu": n_fn_rank, "t_n_per_gpu": n_fn_rank // 64,
                    "l2": "inputs larger than L2 (field %.2f GB per copy)"
                          % (n_fn_rank / 64 * 19 * 64 * n_d / 1e9),
-                   "parallelism": f"slab{world}" if world > 1 else "single"},
+                   "parallelism": f"slab{world}" if world > 1 else "single",
+                   "halo": args.transport_used if world > 1 else None,
+                   "shared_gpu_test_mode": bool(shared)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": alg_bytes,
@@ -370,6 +392,8 @@ def run_b200(args):
         "gpu_launches": args.steps * runner.launches_per_step(),
     }
     if not args.no_e2e:
+        if runner.ipc is not None:
+            runner.ipc.close()
         del runner
         torch.cuda.empty_cache()
         line["e2e"] = e2e_run(args, torch, workloads.channel_z(args.edge, args.edge * world), world,

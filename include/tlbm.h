@@ -151,9 +151,33 @@ typedef struct {
     uint32_t *flags;             /* device status word (OR-ed), may be NULL */
     int rel32;                   /* 1: every |nbr[t][k] - t| * 1216 < 2^31, so the
                                     kernel may use 32-bit relative offsets */
+    /* fused halo (multi-GPU slabs, may be NULL): post-collision values of the
+     * e_z=+1 directions on plane z=3 of tiles [halo_up_begin, halo_up_end) are
+     * also stored to halo_up + (tile - halo_up_begin) * 19 * 64 (+ the usual
+     * in-block offset) -- a neighbour's ghost tiles in peer memory; likewise
+     * e_z=-1 / plane z=0 to halo_down. */
+    void *halo_up;
+    int64_t halo_up_begin, halo_up_end;
+    void *halo_down;
+    int64_t halo_down_begin, halo_down_end;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);
+
+/* ---- peer memory for the fused halo (csrc/peer.cu) ---------------------- */
+/* CUDA IPC export of a device pointer: 64-byte handle + offset of d_ptr in
+ * its allocation; import maps a neighbour's allocation and returns the
+ * pointer at that offset (close with the mapping base = ptr - offset). */
+int tlbm_ipc_export(void *d_ptr, void *h_handle, uint64_t *h_offset);
+int tlbm_ipc_import(const void *h_handle, uint64_t offset, void **d_ptr);
+int tlbm_ipc_close(void *d_base);
+/* Stream-ordered step barrier between slab neighbours: wait until all n
+ * inbox counters >= value (acquire, system scope; sets *d_error and returns
+ * after timeout_ns instead of hanging), and publish value into up to two
+ * neighbours' inbox slots after a system-scope fence. */
+int tlbm_peer_wait(const uint64_t *d_inbox, int n, uint64_t value, uint64_t timeout_ns,
+                   uint32_t *d_error, void *stream);
+int tlbm_peer_signal(uint64_t *d_peer_a, uint64_t *d_peer_b, uint64_t value, void *stream);
 
 #ifdef __cplusplus
 }

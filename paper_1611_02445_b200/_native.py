@@ -29,7 +29,9 @@ class StepArgs(ctypes.Structure):
                 ("t_n", c_i64), ("tile_begin", c_i64), ("tile_end", c_i64),
                 ("f_src", c_vp), ("f_dst", c_vp), ("nbr", c_vp), ("meta", c_vp),
                 ("tau", c_dbl), ("inlet_u", c_dbl * 3), ("outlet_rho", c_dbl),
-                ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int)]
+                ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int),
+                ("halo_up", c_vp), ("halo_up_begin", c_i64), ("halo_up_end", c_i64),
+                ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64)]
 
 
 _PROTOS = {
@@ -64,6 +66,11 @@ _PROTOS = {
                             c_dbl, c_dbl, c_vp, c_vp]),
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
+    "tlbm_ipc_export": (c_int, [c_vp, c_vp, ctypes.POINTER(ctypes.c_uint64)]),
+    "tlbm_ipc_import": (c_int, [c_vp, ctypes.c_uint64, ctypes.POINTER(c_vp)]),
+    "tlbm_ipc_close": (c_int, [c_vp]),
+    "tlbm_peer_wait": (c_int, [c_vp, c_int, ctypes.c_uint64, ctypes.c_uint64, c_vp, c_vp]),
+    "tlbm_peer_signal": (c_int, [c_vp, c_vp, ctypes.c_uint64, c_vp]),
 }
 
 EXPORTED = tuple(_PROTOS)

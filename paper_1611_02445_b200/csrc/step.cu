@@ -33,7 +33,17 @@ struct StepParams {
     double outlet_rho;
     double guard_sq;        // |u|^2 threshold of the guard (+inf: off)
     uint32_t *flags;
+    // fused halo: post-collision outgoing z planes also stored into a
+    // neighbour's ghost tiles (peer memory), tile t -> dst + (t - begin) * 1216
+    T *halo_up;             // e_z = +1 directions of plane z = 3
+    long long halo_up_begin, halo_up_end;
+    T *halo_down;           // e_z = -1 directions of plane z = 0
+    long long halo_down_begin, halo_down_end;
 };
+
+__host__ __device__ constexpr int up_dir(int k) {
+    return k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 13 : k == 3 ? 15 : 17;
+}
 
 constexpr int TILE_VALUES = Q * 64;
 
@@ -129,6 +139,21 @@ step_kernel(const StepParams<T> p) {
         T *out = p.dst + own;
 #pragma unroll
         for (int q = 0; q < Q; ++q) store_out(out + (q * 64 + slot_of<TABLE>(q, x, y, z)), g[q]);
+        if (VARIANT == TLBM_FULL && p.halo_up && z == 3 && tile >= p.halo_up_begin &&
+            tile < p.halo_up_end) {
+            T *peer = p.halo_up + (tile - p.halo_up_begin) * TILE_VALUES;
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                peer[up_dir(k) * 64 + slot_of<TABLE>(up_dir(k), x, y, 3)] = g[up_dir(k)];
+        }
+        if (VARIANT == TLBM_FULL && p.halo_down && z == 0 && tile >= p.halo_down_begin &&
+            tile < p.halo_down_end) {
+            T *peer = p.halo_down + (tile - p.halo_down_begin) * TILE_VALUES;
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                peer[opp(up_dir(k)) * 64 + slot_of<TABLE>(opp(up_dir(k)), x, y, 0)] =
+                    g[opp(up_dir(k))];
+        }
     }
     if (p.flags) {
         // one atomic per warp, and only for bits not yet set: a flow sitting at
@@ -166,6 +191,12 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     p.outlet_rho = a->outlet_rho;
     p.guard_sq = a->u_guard > 0.0 ? a->u_guard * a->u_guard : HUGE_VAL;
     p.flags = a->flags;
+    p.halo_up = static_cast<T *>(a->halo_up);
+    p.halo_up_begin = a->halo_up_begin;
+    p.halo_up_end = a->halo_up_end;
+    p.halo_down = static_cast<T *>(a->halo_down);
+    p.halo_down_begin = a->halo_down_begin;
+    p.halo_down_end = a->halo_down_end;
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32>

@@ -26,6 +26,8 @@ results are bit-identical to the single-domain run (tests).
 
 from dataclasses import dataclass
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -233,6 +235,125 @@ class NcclHalo:
             q.wait()
 
 
+def _export(t):
+    h = (ctypes.c_char * 64)()
+    off = ctypes.c_uint64(0)
+    nat.call("tlbm_ipc_export", nat.ptr(t), h, ctypes.byref(off))
+    return bytes(h), int(off.value)
+
+
+def _import(handle, offset):
+    p = ctypes.c_void_p(0)
+    buf = (ctypes.c_char * 64).from_buffer_copy(handle)
+    nat.call("tlbm_ipc_import", buf, ctypes.c_uint64(offset), ctypes.byref(p))
+    return int(p.value), int(p.value) - offset          # (pointer, mapping base)
+
+
+class IpcHalo:
+    """Fused halo over peer memory (CUDA IPC; NVLink between GPUs).
+
+    The boundary-layer step kernel stores its outgoing z planes directly
+    into the neighbours' ghost tiles (tlbm_step_args.halo_*): no pack kernel,
+    no staging buffer, no copy engine, no NCCL on the step path.  Ordering is
+    a stream-ordered step counter per neighbour pair: before step t a rank
+    waits (tlbm_peer_wait) until both neighbours published t, i.e. finished
+    step t-1 -- so their ghost planes of the copy it reads are written, and
+    they no longer read the copy whose ghosts it is about to write -- and after
+    step t it publishes t+1 into their inboxes (tlbm_peer_signal, system-scope
+    fence first).  A wait that exceeds ``timeout_s`` sets an error word and
+    returns (checked by ``check``) instead of hanging the GPU.
+    """
+
+    def __init__(self, slab, timeout_s=30.0):
+        import torch.distributed as dist
+        self.dist, self.slab = dist, slab
+        s = slab.solver
+        r = slab.range
+        self.esize = s.store.flat.element_size()
+        self.inbox = torch.zeros(2, dtype=torch.int64, device=s.device)  # [from lower, upper]
+        self.error = torch.zeros(1, dtype=torch.int32, device=s.device)
+        self.timeout_ns = int(timeout_s * 1e9)
+        info = {"t_n": s.t_n, "ghost_lo": slab.ghost_lo, "ghost_hi": slab.ghost_hi,
+                "top": slab.top, "bottom": slab.bottom, "esize": self.esize,
+                "store": _export(s.store.flat), "inbox": _export(self.inbox)}
+        torch.cuda.synchronize()
+        infos = [None] * slab.plan.world
+        dist.all_gather_object(infos, info)
+        self.bases = []
+        mapped = {}
+        for nb in sorted({r.lower, r.upper} - {-1}):
+            store, b1 = _import(*infos[nb]["store"])
+            inbox, b2 = _import(*infos[nb]["inbox"])
+            mapped[nb] = (store, inbox)
+            self.bases += [b1, b2]
+        tv = 19 * 64 * self.esize
+        self.up = None
+        if r.upper >= 0:
+            u = infos[r.upper]
+            if u["ghost_lo"][1] - u["ghost_lo"][0] != slab.top[1] - slab.top[0]:
+                raise AssertionError("top layer and upper ghost layer differ")
+            self.up = (mapped[r.upper][0] + u["ghost_lo"][0] * tv, u["t_n"] * tv,
+                       mapped[r.upper][1] + 0)              # -> upper's "from lower" slot
+        self.down = None
+        if r.lower >= 0:
+            lo = infos[r.lower]
+            if lo["ghost_hi"][1] - lo["ghost_hi"][0] != slab.bottom[1] - slab.bottom[0]:
+                raise AssertionError("bottom layer and lower ghost layer differ")
+            self.down = (mapped[r.lower][0] + lo["ghost_hi"][0] * tv, lo["t_n"] * tv,
+                         mapped[r.lower][1] + 8)            # -> lower's "from upper" slot
+        base = self.inbox.data_ptr()
+        if r.lower >= 0 and r.upper >= 0:
+            self.wait_ptr, self.wait_n = base, 2
+        elif r.lower >= 0:
+            self.wait_ptr, self.wait_n = base, 1
+        elif r.upper >= 0:
+            self.wait_ptr, self.wait_n = base + 8, 1
+        else:
+            self.wait_ptr, self.wait_n = base, 0
+        dist.barrier()
+
+    def wait(self, value):
+        s = self.slab.solver
+        nat.call("tlbm_peer_wait", nat.c_vp(self.wait_ptr), self.wait_n, ctypes.c_uint64(value),
+                 ctypes.c_uint64(self.timeout_ns), nat.ptr(self.error), nat.stream_ptr(s.device))
+
+    def arm(self):
+        """Point the step args' halo fields at the neighbours' ghost tiles of
+        the copy this step writes (parity is the same on every rank)."""
+        sl, a = self.slab, self.slab.solver._args
+        dst_copy = 1 - sl.solver.parity
+        if self.up is not None:
+            ghost, copy_bytes, _ = self.up
+            a.halo_up = ghost + dst_copy * copy_bytes
+            a.halo_up_begin, a.halo_up_end = sl.top
+        if self.down is not None:
+            ghost, copy_bytes, _ = self.down
+            a.halo_down = ghost + dst_copy * copy_bytes
+            a.halo_down_begin, a.halo_down_end = sl.bottom
+
+    def disarm(self):
+        a = self.slab.solver._args
+        a.halo_up = a.halo_down = None
+
+    def signal(self, value):
+        s = self.slab.solver
+        pa = self.up[2] if self.up is not None else None
+        pb = self.down[2] if self.down is not None else None
+        nat.call("tlbm_peer_signal", nat.c_vp(pa), nat.c_vp(pb), ctypes.c_uint64(value),
+                 nat.stream_ptr(s.device))
+
+    def check(self):
+        if int(self.error.item()):
+            raise RuntimeError("slab neighbour did not reach the step within the timeout")
+
+    def close(self):
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        for b in self.bases:
+            nat.call("tlbm_ipc_close", nat.c_vp(b))
+        self.bases = []
+
+
 class HostStagedHalo(NcclHalo):
     """The same exchange through host memory over a CPU process group (gloo):
     lets several ranks share one GPU in tests of the multi-process path."""
@@ -277,8 +398,16 @@ class DistributedSlabRunner:
     def __init__(self, geometry, world, rank, config=None, device=None, transport="nccl"):
         self.plan = SlabPlan(geometry, world)
         self.slab = SlabSolver(geometry, self.plan, rank, config, device)
-        halo_cls = HostStagedHalo if transport == "gloo" else NcclHalo
-        self.halo = halo_cls(self.slab) if world > 1 else None
+        self.transport = transport
+        self.ipc = None
+        self.halo = None
+        if world > 1:
+            import torch.distributed as dist
+            staged = transport == "gloo" or (transport == "ipc" and
+                                              dist.get_backend() == "gloo")
+            self.halo = (HostStagedHalo if staged else NcclHalo)(self.slab)
+            if transport == "ipc":
+                self.ipc = IpcHalo(self.slab)
         self.n_fn_owned = self.slab.n_fn_owned
 
     def launches_per_step(self):
@@ -286,6 +415,9 @@ class DistributedSlabRunner:
         sl = self.slab
         if self.halo is None:
             return 1
+        if self.ipc is not None:
+            n = 1 if sl.top == sl.bottom else 2
+            return n + int(sl.interior[1] > sl.interior[0]) + 2     # + wait + signal
         n = 1 if sl.top == sl.bottom else 2
         n += int(sl.interior[1] > sl.interior[0])
         n += sum(b is not None for b in (sl.send_up, sl.send_down, sl.recv_lo, sl.recv_hi))
@@ -305,6 +437,16 @@ class DistributedSlabRunner:
         for _ in range(int(n)):
             if self.halo is None:
                 sl._launch(sl.own)
+                sl.finish()
+                continue
+            if self.ipc is not None:
+                it = sl.solver.iteration
+                self.ipc.wait(it)
+                self.ipc.arm()
+                sl.step_boundary()
+                self.ipc.disarm()
+                sl.step_interior()
+                self.ipc.signal(it + 1)
                 sl.finish()
                 continue
             sl.step_boundary()

@@ -97,7 +97,7 @@ def test_slab_channel_single_rank_runs():
     assert run.n_fn_owned == 32 ** 3 and s.iteration == 5
 
 
-def _mp_worker(rank, world, port, steps, out):
+def _mp_worker(rank, world, port, steps, out, transport="gloo"):
     import os
 
     import torch.distributed as dist
@@ -106,24 +106,34 @@ def _mp_worker(rank, world, port, steps, out):
     torch.cuda.set_device(0)
     geo = CASES["pack_io"]()
     cfg = solver.SimulationConfig(u_max_guard=0.0)
-    run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport="gloo")
+    run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport=transport)
     s = run.slab.solver
     f0 = _f0(geo, np.float64)
     fl = _local_f(f0, run.slab.range, geo.shape[2])
     s.set_fields_canonical(dense.to_canonical(fl, s.tile_grid.non_empty, np.zeros(19)))
+    if run.ipc is not None:
+        run.exchange_current()
     run.step(steps)
+    if run.ipc is not None:
+        run.ipc.check()
     d = s.to_dense(s.fields_canonical(device=True))
     lo = TILE if run.slab.range.lower >= 0 else 0
     r = run.slab.range
     out[rank] = (r.z0, r.z1, d[..., lo:lo + r.z1 - r.z0].cpu().numpy())
+    if run.ipc is not None:
+        run.ipc.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("transport", ["gloo", "ipc"])
 @pytest.mark.parametrize("world", [2, 3])
-def test_multiprocess_runner_gloo_on_one_gpu(world):
-    """DistributedSlabRunner in `world` processes sharing cuda:0 (halo staged
-    through host memory over gloo) == the single-domain step."""
+def test_multiprocess_runner_on_one_gpu(world, transport):
+    """DistributedSlabRunner in `world` processes sharing cuda:0 == the
+    single-domain step.  transport "gloo": halo staged through host memory;
+    "ipc": the fused peer-store halo over CUDA IPC mappings with the
+    stream-ordered step counters (the multi-GPU product path, here with all
+    peers on one device)."""
     import socket
 
     import torch.multiprocessing as mp
@@ -133,7 +143,7 @@ def test_multiprocess_runner_gloo_on_one_gpu(world):
     steps = 10
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, steps, out))
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, steps, out, transport))
              for r in range(world)]
     for p in procs:
         p.start()
