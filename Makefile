@@ -11,11 +11,18 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  ?= -O3 -std=c++20 $(ARCH) -lineinfo -fmad=false -Xptxas -v \
             -Xcompiler -fPIC -Iinclude --expt-relaxed-constexpr
 
-all: $(LIB) oracle
+all: oracle
+	$(MAKE) -j8 $(LIB)
 
-$(LIB): $(SRC) $(HDR)
-	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> $(PKG)/lib/ptxas.log || (cat $(PKG)/lib/ptxas.log; false)
+OBJ      := $(patsubst $(PKG)/csrc/%.cu,$(PKG)/lib/obj/%.o,$(SRC))
+
+$(PKG)/lib/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p $(PKG)/lib/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.log || (cat $@.log; false)
+
+$(LIB): $(OBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJ)
+	@cat $(PKG)/lib/obj/*.o.log > $(PKG)/lib/ptxas.log
 
 oracle:
 	$(MAKE) -s -C oracle

@@ -35,6 +35,7 @@ extern "C" {
 
 enum { TLBM_F64 = 0, TLBM_F32 = 1 };
 enum { TLBM_INCOMPRESSIBLE = 0, TLBM_QUASI = 1 };
+enum { TLBM_LBGK = 0, TLBM_MRT = 1 };   /* collision.py:33-35 CollisionModel */
 enum { TLBM_TABLE_XYZ = 0, TLBM_TABLE_OPTIMIZED = 1, TLBM_TABLE_B200 = 2 };
 enum { TLBM_OK = 0, TLBM_ERR_ARG = 1, TLBM_ERR_CUDA = 2 };
 /* step variants (SPEC.md:531-539 bench ladder) */
@@ -118,6 +119,10 @@ int tlbm_equilibrium(const void *d_rho, const void *d_u, int dtype, int fluid,
 /* collide_lbgk on (19, n) canonical populations in place (collision.py:124). */
 int tlbm_collide_lbgk(void *d_f, int dtype, int fluid, int64_t n, double tau,
                       uint32_t *d_flags, void *stream);
+/* collide_mrt on (19, n) canonical populations in place with the host
+ * float64 19x19 operator h_op (collision.py:234-247). */
+int tlbm_collide_mrt(void *d_f, int dtype, int fluid, int64_t n, const double *h_op,
+                     uint32_t *d_flags, void *stream);
 /* Zou-He closure in place on (19, m) canonical populations of nodes on one
  * face (face = 2*axis + (0 low | 1 high)); kind 0 = velocity inlet with
  * (ux,uy,uz) (boundaries.py:139-157), 1 = pressure outlet with rho0
@@ -160,6 +165,10 @@ typedef struct {
     int64_t halo_up_begin, halo_up_end;
     void *halo_down;
     int64_t halo_down_begin, halo_down_end;
+    int collision;               /* TLBM_LBGK or TLBM_MRT */
+    const double *mrt_op;        /* MRT: host 19x19 float64 operator M^-1 S M,
+                                    row-major (collision.py:206-213); cast to
+                                    the working dtype like op.astype(dtype) */
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);

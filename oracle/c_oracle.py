@@ -21,7 +21,7 @@ class _Params(ctypes.Structure):
                 ("periodic", ctypes.c_int * 3), ("quasi", ctypes.c_int),
                 ("tau", ctypes.c_double), ("inlet_u", ctypes.c_double * 3),
                 ("outlet_rho", ctypes.c_double), ("u_guard", ctypes.c_double),
-                ("nthreads", ctypes.c_int)]
+                ("nthreads", ctypes.c_int), ("mrt_op", ctypes.c_void_p)]
 
 
 _lib = None
@@ -55,7 +55,7 @@ class DenseOracle:
 
     def __init__(self, types, model, tau, inlet_velocity=(0.0, 0.0, 0.0),
                  outlet_density=1.0, periodic=(False, False, False), f0=None,
-                 dtype=np.float64, nthreads=0, u_guard=0.0):
+                 dtype=np.float64, nthreads=0, u_guard=0.0, mrt_operator=None):
         self.types = np.ascontiguousarray(types, dtype=np.uint8)
         self.faces = np.ascontiguousarray(face_ids(self.types, periodic))
         self.dtype = np.dtype(dtype)
@@ -73,6 +73,10 @@ class DenseOracle:
         p.outlet_rho = float(outlet_density)
         p.u_guard = float(u_guard)
         p.nthreads = int(nthreads)
+        self.mrt_op = None
+        if mrt_operator is not None:
+            self.mrt_op = np.ascontiguousarray(mrt_operator, dtype=self.dtype)
+            p.mrt_op = self.mrt_op.ctypes.data
         self.params = p
         self.last_status = 0
         self.failed_step = -1

@@ -85,15 +85,20 @@ def gather(f, types, periodic=(False, False, False)):
 
 def step(f, types, model, tau, inlet_velocity=(0.0, 0.0, 0.0),
          outlet_density=1.0, periodic=(False, False, False), faces=None,
-         iteration=None):
-    """One step on dense f of shape (19, nx, ny, nz); returns the new copy."""
+         iteration=None, mrt_operator=None):
+    """One step on dense f of shape (19, nx, ny, nz); returns the new copy.
+    ``mrt_operator`` (19x19) selects MRT collision (collision.py:234-247)."""
     if faces is None:
         faces = face_ids(types, periodic)
+    if mrt_operator is None:
+        collide = lambda g: nm.collide_lbgk(model, g, tau)  # noqa: E731
+    else:
+        collide = lambda g: nm.collide_mrt(model, g, operator=mrt_operator)  # noqa: E731
     g = gather(f, types, periodic)
     new = f.copy()
     fl = types == FLUID
     try:
-        new[:, fl] = nm.collide_lbgk(model, g[:, fl], tau)
+        new[:, fl] = collide(g[:, fl])
         bb = types == BB_WALL
         new[:, bb] = g[nm.OPP][:, bb]
         for fid in range(6):
@@ -107,7 +112,7 @@ def step(f, types, model, tau, inlet_velocity=(0.0, 0.0, 0.0),
                     nm.zou_he_velocity(sub, c, inlet_velocity, model)
                 else:
                     nm.zou_he_pressure(sub, c, outlet_density, model)
-                new[:, m] = nm.collide_lbgk(model, sub, tau)
+                new[:, m] = collide(sub)
     except nm.OracleDivergence as exc:
         raise nm.OracleDivergence(str(exc), iteration) from None
     ns = types != SOLID

@@ -188,3 +188,69 @@ def zou_he_pressure(g, c, rho0, model):
     j[c["axis"]] = T(c["sign"]) * jn
     _close(g, c, j)
     return jn
+
+
+# -- MRT (collision.py:133-247) ------------------------------------------------
+
+def moment_rows():
+    """Orthogonal D3Q19 moment basis in the reference's row order
+    (collision.py:133-161)."""
+    ex, ey, ez = E[:, 0], E[:, 1], E[:, 2]
+    e2 = ex * ex + ey * ey + ez * ez
+    r = [np.ones(19, dtype=np.int64), 19 * e2 - 30, (21 * e2 * e2 - 53 * e2 + 24) // 2]
+    for ea in (ex, ey, ez):
+        r += [ea, (5 * e2 - 9) * ea]
+    r += [3 * ex * ex - e2, (3 * e2 - 5) * (3 * ex * ex - e2), ey * ey - ez * ez,
+          (3 * e2 - 5) * (ey * ey - ez * ez), ex * ey, ey * ez, ex * ez,
+          (ey * ey - ez * ez) * ex, (ez * ez - ex * ex) * ey, (ex * ex - ey * ey) * ez]
+    return np.stack(r)
+
+
+MOMENTS = moment_rows()
+STRESS = (9, 11, 13, 14, 15)
+
+
+def default_mrt_rates(tau):
+    """collision.py:186-203."""
+    if tau <= 0.5:
+        raise ValueError(f"relaxation time must exceed 0.5: {tau}")
+    s = np.zeros(19)
+    s[1], s[2] = 1.19, 1.4
+    s[4] = s[6] = s[8] = 1.2
+    s[10] = s[12] = 1.4
+    for i in STRESS:
+        s[i] = 1.0 / tau
+    s[16] = s[17] = s[18] = 1.98
+    return s
+
+
+def mrt_operator(rates, dtype=np.float64):
+    """M^-1 diag(s) M in float64 via numpy matmul, cast (collision.py:206-213)."""
+    m = MOMENTS.astype(np.float64)
+    inv = m.T / (m * m).sum(axis=1)
+    rates = np.asarray(rates, dtype=np.float64)
+    return (inv @ (rates[:, None] * m)).astype(dtype)
+
+
+def apply_operator(op, delta):
+    """Fixed-order accumulation skipping zero coefficients (collision.py:216-231)."""
+    out = np.empty_like(delta)
+    for i in range(19):
+        acc = np.zeros_like(delta[0])
+        for j in range(19):
+            c = op[i][j]
+            if c != 0.0:
+                acc += c * delta[j]
+        out[i] = acc
+    return out
+
+
+def collide_mrt(model, f, rates=None, operator=None):
+    f = np.asarray(f)
+    if operator is None:
+        if rates is None:
+            raise ValueError("either moment rates or a precomputed operator is required")
+        operator = mrt_operator(rates, dtype=f.dtype)
+    rho, u, _ = macroscopic(model, f)
+    feq = equilibrium(model, rho, u)
+    return f + apply_operator(operator, feq - f)

@@ -40,6 +40,51 @@ static int CAT(collide, SFX)(const REAL *g, REAL *out, int quasi, REAL inv_tau,
     return st;
 }
 
+/* collide_mrt (collision.py:216-247): g + apply_operator(op, feq - g), the
+ * operator rows accumulated from 0 in column order, zero coefficients
+ * skipped. */
+static int CAT(collide_mrt, SFX)(const REAL *g, REAL *out, int quasi, const REAL *op,
+                                 double u_guard) {
+    REAL rho = g[0];
+    for (int q = 1; q < 19; ++q) rho += g[q];
+    REAL j[3];
+    for (int a = 0; a < 3; ++a) {
+        REAL acc = (REAL)0;
+        for (int q = 0; q < 19; ++q) {
+            if (EV[q][a] == 1) acc += g[q];
+            else if (EV[q][a] == -1) acc -= g[q];
+        }
+        j[a] = acc;
+    }
+    int st = 0;
+    if (rho != rho || (quasi && !(rho > (REAL)0))) st |= 1;
+    REAL u[3];
+    for (int a = 0; a < 3; ++a) u[a] = quasi ? j[a] / rho : j[a];
+    REAL usq = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    if (u_guard > 0 && usq > (REAL)(u_guard * u_guard)) st |= 2;
+    REAL delta[19];
+    for (int q = 0; q < 19; ++q) {
+        REAL cu = (REAL)0;
+        for (int a = 0; a < 3; ++a) {
+            if (EV[q][a] > 0) cu += u[a];
+            else if (EV[q][a] < 0) cu += -u[a];
+        }
+        REAL br = (REAL)3.0 * cu + (REAL)4.5 * cu * cu - (REAL)1.5 * usq;
+        REAL w = (REAL)(q == 0 ? 1.0 / 3.0 : (q < 7 ? 1.0 / 18.0 : 1.0 / 36.0));
+        REAL feq = quasi ? w * (rho * ((REAL)1.0 + br)) : w * (rho + br);
+        delta[q] = feq - g[q];
+    }
+    for (int i = 0; i < 19; ++i) {
+        REAL acc = (REAL)0;
+        for (int k = 0; k < 19; ++k) {
+            REAL c = op[i * 19 + k];
+            if (c != (REAL)0) acc += c * delta[k];
+        }
+        out[i] = g[i] + acc;
+    }
+    return st;
+}
+
 static REAL CAT(osum, SFX)(const REAL *g, const int *d, int n) {
     REAL acc = g[d[0]];
     for (int i = 1; i < n; ++i) acc += g[d[i]];
@@ -138,7 +183,11 @@ int CAT(oracle_step, SFX)(const REAL *f, REAL *fnew, const uint8_t *types,
                         CAT(zh_velocity, SFX)(g, &FACES[faces[n]], p->inlet_u, p->quasi);
                     else if (tag == 4)
                         CAT(zh_pressure, SFX)(g, &FACES[faces[n]], p->outlet_rho);
-                    status |= CAT(collide, SFX)(g, out, p->quasi, inv_tau, p->u_guard);
+                    if (p->mrt_op)
+                        status |= CAT(collide_mrt, SFX)(g, out, p->quasi,
+                                                        (const REAL *)p->mrt_op, p->u_guard);
+                    else
+                        status |= CAT(collide, SFX)(g, out, p->quasi, inv_tau, p->u_guard);
                 }
                 for (int q = 0; q < 19; ++q) fnew[(int64_t)q * N + n] = out[q];
             }

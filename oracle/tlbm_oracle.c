@@ -27,6 +27,7 @@ typedef struct {
     double outlet_rho;
     double u_guard;         /* |u| > u_guard sets flag bit 1 (0 disables) */
     int nthreads;
+    const void *mrt_op;     /* NULL: LBGK; else 19x19 REAL MRT operator, row-major */
 } oracle_params;
 
 static const int EV[19][3] = {

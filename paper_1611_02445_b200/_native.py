@@ -18,6 +18,7 @@ F64, F32 = 0, 1
 INCOMPRESSIBLE, QUASI = 0, 1
 TABLE_XYZ, TABLE_OPTIMIZED, TABLE_B200 = 0, 1, 2
 FULL, PROPAGATION_ONLY, READ_WRITE_ONLY = 0, 1, 2
+LBGK, MRT = 0, 1
 FLAG_DIVERGED, FLAG_GUARD = 1, 2
 
 c_int, c_i64, c_dbl, c_vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -31,7 +32,8 @@ class StepArgs(ctypes.Structure):
                 ("tau", c_dbl), ("inlet_u", c_dbl * 3), ("outlet_rho", c_dbl),
                 ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int),
                 ("halo_up", c_vp), ("halo_up_begin", c_i64), ("halo_up_end", c_i64),
-                ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64)]
+                ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
+                ("collision", c_int), ("mrt_op", c_vp)]
 
 
 _PROTOS = {
@@ -62,6 +64,7 @@ _PROTOS = {
                                            c_vp, c_vp, c_vp]),
     "tlbm_equilibrium": (c_int, [c_vp, c_vp, c_int, c_int, c_i64, c_vp, c_vp]),
     "tlbm_collide_lbgk": (c_int, [c_vp, c_int, c_int, c_i64, c_dbl, c_vp, c_vp]),
+    "tlbm_collide_mrt": (c_int, [c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp]),
     "tlbm_zou_he": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_i64, c_dbl, c_dbl,
                             c_dbl, c_dbl, c_vp, c_vp]),
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),

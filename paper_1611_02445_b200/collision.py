@@ -6,8 +6,11 @@ reference's exact operation order (csrc/physics.cuh), so results are
 bit-identical to the reference.  Inputs may be numpy arrays (results come back
 as numpy) or CUDA tensors (results stay on the device).
 
-Not provided: MRT (collision.py:133-247) -- out of scope for the LBGK hot
-path (SURVEY section 8(f)-1 "next").
+MRT (collision.py:133-247): the moment basis, rates and the
+19x19 velocity-space operator are host setup in float64 numpy exactly as in
+the reference; ``collide_mrt`` and the solver's MRT step apply the operator in
+libtlbm (dense 19 x 19 product, coefficients in the kernel-parameter constant
+bank, reference accumulation order).
 """
 
 import enum
@@ -134,3 +137,77 @@ def reflect(f):
         return f[torch.as_tensor(OPPOSITE, device=f.device)]
     ft, _ = _to_device(f)
     return ft[torch.as_tensor(OPPOSITE, device=ft.device)].cpu().numpy()
+
+
+# -- MRT ----------------------------------------------------------------------
+
+def _moment_rows():
+    """Orthogonal D3Q19 moment basis, reference row order (collision.py:133-161):
+    rho, e, eps, (j, q) per axis, 3pxx, 3pixx, pww, piww, pxy, pyz, pxz, mx,
+    my, mz."""
+    from .lattice import E_VECTORS
+    ex, ey, ez = (E_VECTORS[:, a].astype(np.int64) for a in range(3))
+    e2 = ex * ex + ey * ey + ez * ez
+    rows = [np.ones(19, dtype=np.int64), 19 * e2 - 30, (21 * e2 * e2 - 53 * e2 + 24) // 2]
+    for ea in (ex, ey, ez):
+        rows += [ea, (5 * e2 - 9) * ea]
+    a_xx, a_ww = 3 * ex * ex - e2, ey * ey - ez * ez
+    rows += [a_xx, (3 * e2 - 5) * a_xx, a_ww, (3 * e2 - 5) * a_ww, ex * ey, ey * ez, ex * ez,
+             a_ww * ex, (ez * ez - ex * ex) * ey, (ex * ex - ey * ey) * ez]
+    return np.stack(rows)
+
+
+MOMENT_NAMES = ("rho", "e", "eps", "jx", "qx", "jy", "qy", "jz", "qz", "3pxx", "3pixx",
+                "pww", "piww", "pxy", "pyz", "pxz", "mx", "my", "mz")
+MOMENT_MATRIX = _moment_rows()
+CONSERVED_MOMENTS = (0, 3, 5, 7)
+STRESS_MOMENTS = (9, 11, 13, 14, 15)
+
+
+def moment_matrix_inverse():
+    """M^T D^-1 by orthogonality (collision.py:179-183)."""
+    m = MOMENT_MATRIX.astype(np.float64)
+    return m.T / (m * m).sum(axis=1)
+
+
+def default_mrt_rates(tau):
+    """Shear modes at 1/tau, the customary fixed rates elsewhere
+    (collision.py:186-203)."""
+    if tau <= 0.5:
+        raise ValueError(f"relaxation time must exceed 0.5: {tau}")
+    s = np.zeros(19)
+    s[1], s[2] = 1.19, 1.4
+    s[[4, 6, 8]] = 1.2
+    s[[10, 12]] = 1.4
+    s[list(STRESS_MOMENTS)] = 1.0 / tau
+    s[[16, 17, 18]] = 1.98
+    return s
+
+
+def mrt_operator(rates, dtype=np.float64):
+    """M^-1 diag(rates) M, float64 then cast (collision.py:206-213)."""
+    rates = np.asarray(rates, dtype=np.float64)
+    if rates.shape != (19,):
+        raise ValueError(f"expected 19 moment rates, got shape {rates.shape}")
+    m = MOMENT_MATRIX.astype(np.float64)
+    return (moment_matrix_inverse() @ (rates[:, None] * m)).astype(dtype)
+
+
+def collide_mrt(model, f, rates=None, operator=None):
+    """f + M^-1 S M (feq - f) (collision.py:234-247) on the GPU."""
+    if operator is None:
+        if rates is None:
+            raise ValueError("either moment rates or a precomputed operator is required")
+        operator = mrt_operator(rates, dtype=np.float64)
+    op = np.ascontiguousarray(np.asarray(operator, dtype=np.float64))
+    ft, as_np = _to_device(f)
+    out = ft.clone()
+    rest = tuple(ft.shape[1:])
+    n = int(np.prod(rest)) if rest else 1
+    flags = _flags(ft.device)
+    code = fluid_code(model)
+    nat.call("tlbm_collide_mrt", nat.ptr(out), nat.code_of(ft.dtype), code, n,
+             op.ctypes.data, nat.ptr(flags), nat.stream_ptr(ft.device))
+    if code == nat.QUASI:
+        _raise_if_diverged(flags, "quasi-compressible flow")
+    return _back(out, as_np)

@@ -124,6 +124,25 @@ __global__ void equilibrium_kernel(const T *rho, const T *u, long long n, T *feq
     }
 }
 
+template <class T>
+struct OpParam {
+    T op[Q * Q];
+};
+
+template <class T, int QUASI>
+__global__ void collide_mrt_kernel(T *f, long long n, const OpParam<T> op, uint32_t *flags) {
+    uint32_t st = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g[q] = f[q * n + i];
+        st |= collide_mrt<T, QUASI>(g, op.op, T(HUGE_VAL));
+#pragma unroll
+        for (int q = 0; q < Q; ++q) f[q * n + i] = g[q];
+    }
+    if (flags && st) atomicOr(flags, st);
+}
+
 template <class T, int QUASI>
 __global__ void collide_kernel(T *f, long long n, double inv_tau, uint32_t *flags) {
     uint32_t st = 0;
@@ -260,6 +279,22 @@ extern "C" int tlbm_collide_lbgk(void *d_f, int dtype, int fluid, int64_t n, dou
         collide_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
             static_cast<T *>(d_f), n, 1.0 / tau, d_flags);
         return launch_check("collide_kernel");
+    });
+}
+
+extern "C" int tlbm_collide_mrt(void *d_f, int dtype, int fluid, int64_t n, const double *h_op,
+                                uint32_t *d_flags, void *stream) {
+    if (!h_op) {
+        set_error("tlbm_collide_mrt: operator required");
+        return TLBM_ERR_ARG;
+    }
+    if (n == 0) return TLBM_OK;
+    return dispatch(dtype, fluid, 0, [&]<class T, int QU, int TB>() {
+        OpParam<T> op;
+        for (int k = 0; k < Q * Q; ++k) op.op[k] = T(h_op[k]);
+        collide_mrt_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+            static_cast<T *>(d_f), n, op, d_flags);
+        return launch_check("collide_mrt_kernel");
     });
 }
 

@@ -123,6 +123,50 @@ __device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, T guard_sq) {
     return status_of<T, QUASI>(rho, usq, guard_sq);
 }
 
+// MRT collide in place: g <- g + A (feq - g) with the velocity-space operator
+// A = M^-1 S M (collision.py:206-247), A row-major in op[19*19].  Rows are
+// accumulated from 0 in column order like apply_operator (collision.py:216-
+// 231).  The reference skips exact-zero coefficients; adding their c * d = 0
+// terms instead leaves every finite result bit-identical (x + 0 = x), so the
+// kernel runs the dense 19 x 19 product with coefficients read straight from
+// the kernel-parameter constant bank (compile-time offsets after unrolling).
+template <class T, int QUASI>
+__device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq) {
+    T rho, u[3];
+    moments<T, QUASI>(g, rho, u);
+    const T usq = speed_sq(u);
+    const T c15 = T(1.5) * usq;
+    T d[Q];
+    d[0] = feq_of<T, QUASI>(0, rho, (T(3.0) * T(0) + T(4.5) * T(0) * T(0)) - c15) - g[0];
+#pragma unroll
+    for (int q = 1; q < Q; ++q) {
+        if (opp(q) < q) continue;
+        const int o = opp(q);
+        T cu = T(0);
+        bool first = true;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int e = e_axis(q, a);
+            if (e == 0) continue;
+            const T term = e > 0 ? u[a] : -u[a];
+            cu = first ? term : cu + term;
+            first = false;
+        }
+        const T A = T(3.0) * cu;
+        const T B = T(4.5) * cu * cu;
+        d[q] = feq_of<T, QUASI>(q, rho, (A + B) - c15) - g[q];
+        d[o] = feq_of<T, QUASI>(o, rho, (B - A) - c15) - g[o];
+    }
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        T acc = T(0);
+#pragma unroll
+        for (int j = 0; j < Q; ++j) acc = acc + op[i * Q + j] * d[j];
+        g[i] = g[i] + acc;
+    }
+    return status_of<T, QUASI>(rho, usq, guard_sq);
+}
+
 // ---- Zou-He (boundaries.py:53-92 closures, 132-195 arithmetic) -----------
 // FACE = 2*axis + (0 low face, inward sign +1 | 1 high face, sign -1)
 __host__ __device__ constexpr int face_axis(int face) { return face >> 1; }

@@ -13,215 +13,14 @@
 // 32-byte sector of the source copy is consumed by exactly one destination
 // tile, so DRAM traffic is the 2 x 19 x 8 B / node minimum plus metadata
 // (4 B/node meta word + 108 B/tile neighbour row).
-#include <cmath>
-
+// (kernel and launch templates: step_impl.cuh; instantiated per dtype in
+// step_f64.cu / step_f32.cu; this file validates and dispatches.)
 #include "common.cuh"
-#include "physics.cuh"
+#include "d3q19.cuh"
 
 namespace tlbm {
-namespace {
-
-template <class T>
-struct StepParams {
-    const T *__restrict__ src;
-    T *__restrict__ dst;
-    const int32_t *__restrict__ nbr;
-    const uint32_t *__restrict__ meta;
-    long long tile_begin, tile_end;
-    double inv_tau;
-    double inlet_u[3];
-    double outlet_rho;
-    double guard_sq;        // |u|^2 threshold of the guard (+inf: off)
-    uint32_t *flags;
-    // fused halo: post-collision outgoing z planes also stored into a
-    // neighbour's ghost tiles (peer memory), tile t -> dst + (t - begin) * 1216
-    T *halo_up;             // e_z = +1 directions of plane z = 3
-    long long halo_up_begin, halo_up_end;
-    T *halo_down;           // e_z = -1 directions of plane z = 0
-    long long halo_down_begin, halo_down_end;
-};
-
-__host__ __device__ constexpr int up_dir(int k) {
-    return k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 13 : k == 3 ? 15 : 17;
-}
-
-constexpr int TILE_VALUES = Q * 64;
-
-// 2 tiles (128 threads) per CTA and a 64-register cap (8 CTAs = 32 warps per
-// SM) measured best on B200 for fp64: 0.797 ms / 256^3 channel step vs
-// 0.915 ms at 4 tiles / 78 registers (scripts/step_sweep.py, profiles/).
-#ifndef TLBM_TPC
-#define TLBM_TPC 2
-#endif
-#ifndef TLBM_MINB
-#define TLBM_MINB 8
-#endif
-
-template <class T>
-__device__ __forceinline__ T load_ro(const T *p) { return __ldg(p); }
-
-template <class T>
-__device__ __forceinline__ void store_out(T *p, T v) {
-#ifdef TLBM_STORE_CS
-    __stcs(p, v);
-#else
-    *p = v;
-#endif
-}
-
-// REL32: neighbour rows are staged as 32-bit element offsets relative to the
-// thread's own tile, so every per-direction address is one 32-bit add/select
-// and one IMAD.WIDE from a 64-bit base fixed per thread; valid whenever
-// |nbr - tile| * 1216 < 2^31 (checked on the host, tiling.py), otherwise the
-// 64-bit path recomputes full indices.
-template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32>
-__global__ void __launch_bounds__(64 * TPC, TLBM_MINB)
-step_kernel(const StepParams<T> p) {
-    __shared__ int s_nbr[TPC][NBR];
-    const int ti = threadIdx.x >> 6;
-    const int j = threadIdx.x & 63;
-    const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
-    const long long tile = tile0 + ti;
-
-    if (VARIANT != TLBM_READ_WRITE_ONLY) {
-        for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
-            const long long t = tile0 + i / NBR;
-            const long long nb = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
-            s_nbr[i / NBR][i % NBR] = (int)(REL32 ? (nb >= 0 ? (nb - t) * TILE_VALUES : 0) : nb);
-        }
-        __syncthreads();
-    }
-
-    const uint32_t meta = tile < p.tile_end ? p.meta[tile * 64 + j] : 0u;
-    uint32_t status = 0;
-    if (meta & META_ACTIVE) {
-        const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
-        const long long own = tile * TILE_VALUES;
-        const T *base = p.src + own;
-        T g[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
-                g[q] = load_ro(base + (q * 64 + slot_of<TABLE>(q, x, y, z)));
-                continue;
-            }
-            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
-            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
-            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
-            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
-            const int in_tile = q * 64 + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
-            const int bounced = opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
-            const bool link = (meta >> q) & 1u;
-            if (REL32) {
-                const int rel = (dx | dy | dz) ? s_nbr[ti][delta_index(dx, dy, dz)] : 0;
-                g[q] = load_ro(base + (link ? rel + in_tile : bounced));
-            } else {
-                const long long nb = (dx | dy | dz) ? (long long)s_nbr[ti][delta_index(dx, dy, dz)]
-                                                    : tile;
-                const long long off = link ? nb * TILE_VALUES + in_tile : own + bounced;
-                g[q] = load_ro(p.src + off);
-            }
-        }
-
-        if (VARIANT == TLBM_FULL) {
-            const int tag = meta_type(meta);
-            if (tag == BB_WALL) {
-                // collision.py:250-252 reflect: f_new[q] = g[opp(q)]
-#pragma unroll
-                for (int q = 1; q < Q; ++q)
-                    if (q < opp(q)) { T t = g[q]; g[q] = g[opp(q)]; g[opp(q)] = t; }
-            } else {
-                if (tag == INLET || tag == OUTLET)
-                    zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
-                status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
-            }
-        }
-        T *out = p.dst + own;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) store_out(out + (q * 64 + slot_of<TABLE>(q, x, y, z)), g[q]);
-        if (VARIANT == TLBM_FULL && p.halo_up && z == 3 && tile >= p.halo_up_begin &&
-            tile < p.halo_up_end) {
-            T *peer = p.halo_up + (tile - p.halo_up_begin) * TILE_VALUES;
-#pragma unroll
-            for (int k = 0; k < 5; ++k)
-                peer[up_dir(k) * 64 + slot_of<TABLE>(up_dir(k), x, y, 3)] = g[up_dir(k)];
-        }
-        if (VARIANT == TLBM_FULL && p.halo_down && z == 0 && tile >= p.halo_down_begin &&
-            tile < p.halo_down_end) {
-            T *peer = p.halo_down + (tile - p.halo_down_begin) * TILE_VALUES;
-#pragma unroll
-            for (int k = 0; k < 5; ++k)
-                peer[opp(up_dir(k)) * 64 + slot_of<TABLE>(opp(up_dir(k)), x, y, 0)] =
-                    g[opp(up_dir(k))];
-        }
-    }
-    if (p.flags) {
-        // one atomic per warp, and only for bits not yet set: a flow sitting at
-        // the |u| guard must not serialise every warp on one L2 address
-        const uint32_t any = __reduce_or_sync(0xffffffffu, status);
-        if (any && (threadIdx.x & 31) == 0 &&
-            (any & ~*reinterpret_cast<volatile uint32_t *>(p.flags)))
-            atomicOr(p.flags, any);
-    }
-}
-
-constexpr int TPC = TLBM_TPC;
-
-template <class T, int QUASI, int TABLE, int VARIANT, bool REL32>
-int launch_as(const tlbm_step_args *a, cudaStream_t s);
-
-template <class T, int QUASI, int TABLE, int VARIANT>
-int launch(const tlbm_step_args *a, cudaStream_t s) {
-    if (a->rel32)
-        return launch_as<T, QUASI, TABLE, VARIANT, true>(a, s);
-    return launch_as<T, QUASI, TABLE, VARIANT, false>(a, s);
-}
-
-template <class T, int QUASI, int TABLE, int VARIANT, bool REL32>
-int launch_as(const tlbm_step_args *a, cudaStream_t s) {
-    StepParams<T> p;
-    p.src = static_cast<const T *>(a->f_src);
-    p.dst = static_cast<T *>(a->f_dst);
-    p.nbr = a->nbr;
-    p.meta = a->meta;
-    p.tile_begin = a->tile_begin;
-    p.tile_end = a->tile_end;
-    p.inv_tau = 1.0 / a->tau;
-    for (int k = 0; k < 3; ++k) p.inlet_u[k] = a->inlet_u[k];
-    p.outlet_rho = a->outlet_rho;
-    p.guard_sq = a->u_guard > 0.0 ? a->u_guard * a->u_guard : HUGE_VAL;
-    p.flags = a->flags;
-    p.halo_up = static_cast<T *>(a->halo_up);
-    p.halo_up_begin = a->halo_up_begin;
-    p.halo_up_end = a->halo_up_end;
-    p.halo_down = static_cast<T *>(a->halo_down);
-    p.halo_down_begin = a->halo_down_begin;
-    p.halo_down_end = a->halo_down_end;
-    const long long n = a->tile_end - a->tile_begin;
-    if (n <= 0) return TLBM_OK;
-    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32>
-        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
-    return launch_check("step_kernel");
-}
-
-struct StepLaunch {
-    const tlbm_step_args *a;
-    cudaStream_t s;
-    template <class T, int QUASI, int TABLE>
-    int operator()() const {
-        switch (a->variant) {
-            case TLBM_FULL: return launch<T, QUASI, TABLE, TLBM_FULL>(a, s);
-            case TLBM_PROPAGATION_ONLY:
-                return QUASI ? TLBM_OK : launch<T, 0, TABLE, TLBM_PROPAGATION_ONLY>(a, s);
-            case TLBM_READ_WRITE_ONLY:
-                return QUASI ? TLBM_OK : launch<T, 0, TABLE, TLBM_READ_WRITE_ONLY>(a, s);
-        }
-        set_error("unknown step variant %d", a->variant);
-        return TLBM_ERR_ARG;
-    }
-};
-
-}  // namespace
+int step_launch_f64(const tlbm_step_args *a, cudaStream_t s);
+int step_launch_f32(const tlbm_step_args *a, cudaStream_t s);
 }  // namespace tlbm
 
 using namespace tlbm;
@@ -241,10 +40,22 @@ extern "C" int tlbm_step(const tlbm_step_args *a, void *stream) {
                   (long long)a->tile_begin, (long long)a->tile_end, (long long)a->t_n);
         return TLBM_ERR_ARG;
     }
-    if (!(a->tau > 0.5)) {
+    if (a->collision != TLBM_LBGK && a->collision != TLBM_MRT) {
+        set_error("tlbm_step: unknown collision model %d", a->collision);
+        return TLBM_ERR_ARG;
+    }
+    if (a->collision == TLBM_MRT && !a->mrt_op) {
+        set_error("tlbm_step: MRT needs the 19x19 operator (mrt_op)");
+        return TLBM_ERR_ARG;
+    }
+    if (a->collision == TLBM_LBGK && !(a->tau > 0.5)) {
         set_error("tlbm_step: relaxation time must exceed 0.5, got %g", a->tau);
         return TLBM_ERR_ARG;
     }
-    int fluid = (a->variant == TLBM_FULL) ? a->fluid : TLBM_INCOMPRESSIBLE;
-    return dispatch(a->dtype, fluid, a->table, StepLaunch{a, as_stream(stream)});
+    int rc;
+    if ((rc = check_dtype(a->dtype)) || (rc = check_fluid(a->fluid)) ||
+        (rc = check_table(a->table)))
+        return rc;
+    return a->dtype == TLBM_F64 ? step_launch_f64(a, as_stream(stream))
+                                : step_launch_f32(a, as_stream(stream));
 }

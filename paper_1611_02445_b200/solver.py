@@ -49,6 +49,7 @@ class SimulationConfig:
     precision: str = "f64"
     u_max_guard: float = 0.05
     table: LayoutTable = LayoutTable.B200
+    mrt_matrix: object = None      # optional explicit 19x19 operator (overrides rates)
 
     def __post_init__(self):
         self.collision = CollisionModel(getattr(self.collision, "value", self.collision))
@@ -58,9 +59,26 @@ class SimulationConfig:
             raise ValueError(f"relaxation time must exceed 0.5: {self.tau}")
         if self.precision not in ("f32", "f64"):
             raise ValueError(f"unknown precision: {self.precision!r}")
-        if self.collision is not CollisionModel.LBGK:
-            raise NotImplementedError("only LBGK collision is on the B200 path "
-                                      "(MRT is SURVEY section 8(f)-1 'next')")
+        if self.collision is CollisionModel.MRT:
+            from .collision import default_mrt_rates
+            rates = (default_mrt_rates(self.tau) if self.mrt_relaxation is None
+                     else np.asarray(self.mrt_relaxation, dtype=np.float64))
+            if rates.shape != (19,):
+                raise ValueError("mrt_relaxation needs 19 moment rates")
+            self.mrt_relaxation = tuple(float(r) for r in rates)
+
+    @property
+    def mrt_operator(self):
+        """float64 M^-1 S M of the configured rates (None for LBGK)."""
+        if self.collision is not CollisionModel.MRT:
+            return None
+        if self.mrt_matrix is not None:
+            op = np.asarray(self.mrt_matrix, dtype=np.float64)
+            if op.shape != (19, 19):
+                raise ValueError("mrt_matrix must be 19x19")
+            return op
+        from .collision import mrt_operator
+        return mrt_operator(self.mrt_relaxation, dtype=np.float64)
 
     @property
     def dtype(self):
@@ -110,6 +128,13 @@ class Solver:
         a.outlet_rho = float(geometry.outlet_density)
         a.u_guard = float(self.config.u_max_guard or 0.0)
         a.rel32 = int(self.tiling.rel32)
+        self._mrt_op = self.config.mrt_operator        # kept alive for the ABI pointer
+        if self._mrt_op is not None:
+            self._mrt_op = np.ascontiguousarray(self._mrt_op)
+            a.collision = nat.MRT
+            a.mrt_op = self._mrt_op.ctypes.data
+        else:
+            a.collision = nat.LBGK
         self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
         self.init_equilibrium()
 

@@ -28,9 +28,18 @@ elif a.geometry == "cavity":
 else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0))
-vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY}
+vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY,
+        "mrt": nat.FULL}
 n_d = 8 if a.precision == "f64" else 4
+solvers = {"lbgk": s}
 for v in a.variants.split(","):
+    if v == "mrt" and "mrt" not in solvers:
+        from paper_1611_02445_b200.solver import SimulationConfig, Solver
+        cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision=a.precision,
+                               table=a.table, u_max_guard=0.0)
+        del solvers["lbgk"], s
+        torch.cuda.empty_cache()
+        s = solvers["mrt"] = Solver(geo, cfg)
     s.step(5, variant=vmap[v], check=False)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

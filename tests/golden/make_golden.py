@@ -18,8 +18,9 @@ Everything here calls the reference package ``tilelbm`` (imported from
 * step.npz      -- the step has no reference implementation, so
                    it is composed here from reference functions only
                    (classify_boundary_faces, FACE_CLOSURES, zou_he_*,
-                   collide_lbgk, reflect) following SURVEY Appendix A: a small
-                   sphere pack with inlet/outlet, 6 steps, f64/f32, both fluid
+                   collide_lbgk / collide_mrt, reflect) following SURVEY
+                   Appendix A: a small sphere pack with inlet/outlet, 6 LBGK
+                   steps and 4 MRT steps (default rates), f64/f32, both fluid
                    models.  Pins the oracle and the GPU step to reference
                    arithmetic.
 """
@@ -47,7 +48,9 @@ DTYPES = {"f64": np.float64, "f32": np.float32}
 
 
 def lattice():
-    out = {"e": rl.E_VECTORS, "w": rl.WEIGHTS, "opp": rl.OPPOSITE}
+    out = {"e": rl.E_VECTORS, "w": rl.WEIGHTS, "opp": rl.OPPOSITE,
+           "moments": rc.MOMENT_MATRIX, "mrt_rates_0.6": rc.default_mrt_rates(0.6),
+           "mrt_op_0.6": rc.mrt_operator(rc.default_mrt_rates(0.6))}
     for t in rlay.LayoutTable:
         out[f"perm_{t.value}"] = rlay.table_permutations(t)
     np.savez_compressed(os.path.join(HERE, "lattice.npz"), **out)
@@ -64,6 +67,7 @@ def numerics():
             out[f"rho_{dn}_{mn}"], out[f"u_{dn}_{mn}"], out[f"p_{dn}_{mn}"] = rho, u, p
             out[f"feq_{dn}_{mn}"] = rc.equilibrium(m, rho, u)
             out[f"post_{dn}_{mn}"] = rc.collide_lbgk(m, f, 0.6)
+            out[f"mrt_{dn}_{mn}"] = rc.collide_mrt(m, f, rates=rc.default_mrt_rates(0.6))
             for (axis, sign), c in rb.FACE_CLOSURES.items():
                 key = f"{axis}{'lo' if sign > 0 else 'hi'}"
                 g = f.copy()
@@ -101,7 +105,7 @@ def tiling():
     np.savez_compressed(os.path.join(HERE, "tiling.npz"), **out)
 
 
-def reference_step(f, geometry, model, tau):
+def reference_step(f, geometry, model, tau, mrt=False):
     """One step composed only of reference functions."""
     t = geometry.types
     nx, ny, nz = t.shape
@@ -117,9 +121,14 @@ def reference_step(f, geometry, model, tau):
         src_val[dst] = f[q][src]
         src_ok[dst] = ns[src]
         g[q] = np.where(src_ok, src_val, f[rl.OPPOSITE[q]])
+    if mrt:
+        op = rc.mrt_operator(rc.default_mrt_rates(tau), dtype=f.dtype)
+        collide = lambda h: rc.collide_mrt(model, h, operator=op)  # noqa: E731
+    else:
+        collide = lambda h: rc.collide_lbgk(model, h, tau)  # noqa: E731
     new = f.copy()
     fl = t == rg.NodeType.FLUID
-    new[:, fl] = rc.collide_lbgk(model, g[:, fl], tau)
+    new[:, fl] = collide(g[:, fl])
     bb = t == rg.NodeType.BB_WALL
     new[:, bb] = rc.reflect(g[:, bb])
     for key, (inlet, outlet) in rb.classify_boundary_faces(geometry).items():
@@ -133,7 +142,7 @@ def reference_step(f, geometry, model, tau):
                 rb.zou_he_velocity(sub, c, geometry.inlet_velocity, model)
             else:
                 rb.zou_he_pressure(sub, c, geometry.outlet_density, model)
-            new[(slice(None),) + idx] = rc.collide_lbgk(model, sub, tau)
+            new[(slice(None),) + idx] = collide(sub)
     return new
 
 
@@ -153,10 +162,15 @@ def step():
             u = np.zeros((3,) + geo.shape, dtype=dt)
             u[2] = 0.01
             # f0 = equilibrium(1, (0, 0, 0.01)) * (1 + pert), rebuilt by the tests
-            f = rc.equilibrium(m, rho, u) * (1 + pert).astype(dt)
+            f0 = rc.equilibrium(m, rho, u) * (1 + pert).astype(dt)
+            f = f0
             for _ in range(6):
                 f = reference_step(f, geo, m, 0.6)
             out[f"f6_{dn}_{mn}"] = f
+            f = f0
+            for _ in range(4):
+                f = reference_step(f, geo, m, 0.6, mrt=True)
+            out[f"mrt4_{dn}_{mn}"] = f
     np.savez_compressed(os.path.join(HERE, "step.npz"), **out)
 
 

@@ -97,3 +97,22 @@ def test_init_from_macroscopic(mn):
     r2, u2, p2 = s.macroscopic()
     assert np.array_equal((r2, u2, p2)[0], nm.macroscopic(MODELS[mn], want)[0])
     assert np.array_equal(u2, nm.macroscopic(MODELS[mn], want)[1])
+
+
+@pytest.mark.parametrize("dn", DTYPES)
+@pytest.mark.parametrize("mn", MODELS)
+def test_collide_mrt_golden(golden, dn, mn):
+    g = golden("numerics")
+    f = g[f"f_{dn}"]
+    op = golden("lattice")["mrt_op_0.6"]
+    out = collision.collide_mrt(MODELS[mn], f, operator=op)
+    assert out.dtype == f.dtype
+    assert np.array_equal(out, g[f"mrt_{dn}_{mn}"])
+
+
+def test_mrt_setup_matches_oracle(golden):
+    g = golden("lattice")
+    assert np.array_equal(collision.MOMENT_MATRIX, g["moments"])
+    assert np.array_equal(collision.default_mrt_rates(0.6), g["mrt_rates_0.6"])
+    assert np.allclose(collision.mrt_operator(collision.default_mrt_rates(0.6)),
+                       g["mrt_op_0.6"], rtol=0, atol=1e-15)

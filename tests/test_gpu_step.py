@@ -248,3 +248,79 @@ def test_spec_step_and_run_api():
     w = np.asarray(nm.W)
     f = st2.solver.fields_canonical()
     assert np.array_equal(f, np.broadcast_to(w[:, None, None], f.shape))
+
+
+# -- MRT (SPEC acceptance 8, 9) ---------------------------------
+
+def mrt_config(model, dt, op=None, rates=None, table=layout.LayoutTable.B200):
+    return solver.SimulationConfig(collision="mrt", fluid=model, tau=0.6,
+                                   precision="f64" if dt == np.float64 else "f32",
+                                   table=table, u_max_guard=0.0, mrt_relaxation=rates,
+                                   mrt_matrix=op)
+
+
+@pytest.mark.parametrize("table", list(layout.LayoutTable))
+@pytest.mark.parametrize("dn", DTYPES)
+@pytest.mark.parametrize("mn", MODELS)
+def test_mrt_reference_composed_golden(golden, table, dn, mn):
+    g = golden("step")
+    dt, m = DTYPES[dn], MODELS[mn]
+    geo = geometry.Geometry(g["types"], tuple(g["inlet_velocity"]), float(g["outlet_density"]))
+    rho = np.ones(geo.shape, dtype=dt)
+    u = np.zeros((3,) + geo.shape, dtype=dt)
+    u[2] = 0.01
+    f0 = nm.equilibrium(m, rho, u) * (1 + g["pert"]).astype(dt)
+    s = solver.Solver(geo, mrt_config(m, dt, op=golden("lattice")["mrt_op_0.6"], table=table))
+    s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+    s.step(4)
+    compare(s, g[f"mrt4_{dn}_{mn}"], dt)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_mrt_random_geometries(c_oracle, seed):
+    rng = np.random.default_rng(500 + seed)
+    shape = tuple(int(v) for v in rng.integers(6, 22, size=3))
+    t = random_geometry(rng, shape)
+    geo = geometry.Geometry(t, inlet_velocity=(0.0, 0.01, 0.02), outlet_density=1.0)
+    for dt in (np.float64, np.float32):
+        for m in MODELS.values():
+            cfg = mrt_config(m, dt)
+            f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), seed)
+            o = c_oracle.DenseOracle(t, m, 0.6, geo.inlet_velocity, 1.0, f0=f0, dtype=dt,
+                                     mrt_operator=cfg.mrt_operator.astype(dt))
+            o.run(8)
+            s = solver.Solver(geo, cfg)
+            s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+            s.step(8)
+            compare(s, o.f, dt)
+
+
+def test_mrt_bgk_limit():
+    """SPEC acceptance 9: all moment rates = 1/tau -> MRT == LBGK to 1e-12."""
+    geo = geometry.generate_sphere_pack(24, 6, 0.6, seed=8, inlet_velocity=(0, 0, 0.01))
+    m = MODELS["inc"]
+    f0 = perturbed_eq(geo.shape, m, np.float64, (0.0, 0.0, 0.01), 4)
+    runs = []
+    for coll in ("lbgk", "mrt"):
+        cfg = solver.SimulationConfig(collision=coll, tau=0.6, u_max_guard=0.0,
+                                      mrt_relaxation=np.full(19, 1 / 0.6))
+        s = solver.Solver(geo, cfg)
+        s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+        s.step(10)
+        runs.append(s.fields_canonical()[:, s.nonsolid_mask()])
+    assert rel(runs[1], runs[0]) <= 1e-12
+
+
+@pytest.mark.parametrize("mn", MODELS)
+def test_mrt_sealed_box_mass_conservation(mn):
+    t = np.full((32, 32, 32), 2, np.uint8)
+    t[1:-1, 1:-1, 1:-1] = 1
+    t[12:20, 3:9, 14:30] = 0
+    geo = geometry.Geometry(t)
+    m = MODELS[mn]
+    s = solver.Solver(geo, mrt_config(m, np.float64))
+    s.set_fields_canonical(dense.to_canonical(perturbed_eq(t.shape, m, np.float64, seed=9),
+                                              s.tile_grid.non_empty, nm.W))
+    m0 = s.total_mass()
+    s.run(1000)
+    assert abs(s.total_mass() - m0) / m0 <= 1e-10

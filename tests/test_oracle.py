@@ -19,6 +19,27 @@ MODELS = {"inc": nm.INCOMPRESSIBLE, "quasi": nm.QUASI_COMPRESSIBLE}
 DTYPES = {"f64": np.float64, "f32": np.float32}
 
 
+def test_mrt_setup_golden(golden):
+    g = golden("lattice")
+    assert np.array_equal(nm.MOMENTS, g["moments"])
+    assert np.array_equal(nm.default_mrt_rates(0.6), g["mrt_rates_0.6"])
+    # the operator is a float64 BLAS matmul: equal here, to round-off anywhere
+    op = nm.mrt_operator(nm.default_mrt_rates(0.6))
+    assert np.allclose(op, g["mrt_op_0.6"], rtol=0, atol=1e-15)
+
+
+def test_mrt_matches_live_reference(reference):
+    rc = reference.collision
+    for tau in (0.55, 0.8):
+        assert np.array_equal(rc.mrt_operator(rc.default_mrt_rates(tau)),
+                              nm.mrt_operator(nm.default_mrt_rates(tau)))
+    f = (nm.W[:, None] * np.random.default_rng(3).uniform(0.7, 1.3, (19, 50)))
+    for m in rc.FluidModel:
+        a = rc.collide_mrt(m, f, rates=rc.default_mrt_rates(0.7))
+        b = nm.collide_mrt(m.value, f, rates=nm.default_mrt_rates(0.7))
+        assert np.array_equal(a, b)
+
+
 def test_lattice_golden(golden):
     g = golden("lattice")
     assert np.array_equal(g["e"], nm.E)
@@ -40,6 +61,8 @@ def test_numerics_golden(golden, dn, mn):
         assert got.dtype == ref.dtype and np.array_equal(got, ref), name
     assert np.array_equal(nm.equilibrium(m, rho, u), g[f"feq_{dn}_{mn}"])
     assert np.array_equal(nm.collide_lbgk(m, f, 0.6), g[f"post_{dn}_{mn}"])
+    op = golden("lattice")["mrt_op_0.6"].astype(f.dtype)
+    assert np.array_equal(nm.collide_mrt(m, f, operator=op), g[f"mrt_{dn}_{mn}"])
     for (axis, sign), c in nm.FACES.items():
         key = f"{axis}{'lo' if sign > 0 else 'hi'}"
         h = f.copy()
@@ -110,6 +133,22 @@ def test_dense_oracle_matches_reference_step(golden, dn, mn):
     kw = dict(inlet_velocity=tuple(g["inlet_velocity"]), outlet_density=float(g["outlet_density"]))
     f = dense.run(f, g["types"], m, 0.6, 6, **kw)
     assert np.array_equal(f, g[f"f6_{dn}_{mn}"])
+
+
+@pytest.mark.parametrize("dn", DTYPES)
+@pytest.mark.parametrize("mn", MODELS)
+def test_oracles_match_reference_mrt_step(golden, c_oracle, dn, mn):
+    g = golden("step")
+    dt, m = DTYPES[dn], MODELS[mn]
+    op = golden("lattice")["mrt_op_0.6"].astype(dt)
+    f0 = _golden_step_f0(g, dt, m)
+    kw = dict(inlet_velocity=tuple(g["inlet_velocity"]), outlet_density=float(g["outlet_density"]))
+    f = dense.run(f0, g["types"], m, 0.6, 4, mrt_operator=op, **kw)
+    assert np.array_equal(f, g[f"mrt4_{dn}_{mn}"])
+    o = c_oracle.DenseOracle(g["types"], m, 0.6, f0=f0, dtype=dt, mrt_operator=op, **kw)
+    o.run(4)
+    ns = g["types"] != 0
+    assert np.array_equal(o.f[:, ns], g[f"mrt4_{dn}_{mn}"][:, ns])
 
 
 @pytest.mark.parametrize("dn", DTYPES)
