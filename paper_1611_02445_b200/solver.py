@@ -311,14 +311,45 @@ def step(state):
 
 
 def run(config, geometry, iterations, outputs=None, device=None, check_every=STATUS_RING):
-    """Iterate ``iterations`` steps (SPEC.md:403-410).  Returns
-    (state, diagnostics) with MFLUPS-relevant counts and guard trips.
-    ``outputs``: optional callable(solver) invoked after the run."""
+    """Iterate ``iterations`` steps (SPEC.md:403-410); returns (state,
+    diagnostics).
+
+    ``outputs``: a callable(solver) run at the end, or a dict with any of
+      "convergence_every": k   relative L2 change of u every k steps
+      "tolerance": eps         stop early once that change is below eps
+      "vtk": path, "csv": path write the final rho/u (legacy VTK / CSV slice)
+    Zero iterations return the initial state unchanged.
+    """
+    from .output import ConvergenceEstimator, dense_macroscopic, write_csv_slice, write_vtk
     solver = Solver(geometry, config, device)
-    solver.run(iterations, check_every=check_every)
+    opts = outputs if isinstance(outputs, dict) else {}
+    every = int(opts.get("convergence_every") or 0)
+    tol = opts.get("tolerance")
+    est = ConvergenceEstimator(solver, every) if every > 0 else None
+    if est is not None:
+        est()
+    left = int(iterations)
+    converged = False
+    while left > 0:
+        k = min(left, every if every > 0 else check_every)
+        solver.run(k, check_every=check_every)
+        left -= k
+        if est is not None:
+            change = est()
+            if tol is not None and change is not None and change < tol:
+                converged = True
+                break
     diagnostics = {"iterations": solver.iteration, "t_n": solver.t_n, "n_fn": solver.n_fn,
-                   "guard_iterations": list(solver.guard_iterations)}
-    if outputs is not None:
+                   "guard_iterations": list(solver.guard_iterations),
+                   "convergence": list(est.history) if est is not None else [],
+                   "converged": converged}
+    if opts.get("vtk") or opts.get("csv"):
+        rho, u = dense_macroscopic(solver)
+        if opts.get("vtk"):
+            write_vtk(opts["vtk"], rho, u)
+        if opts.get("csv"):
+            write_csv_slice(opts["csv"], rho, u)
+    if callable(outputs):
         outputs(solver)
     return solver.state, diagnostics
 

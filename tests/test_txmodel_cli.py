@@ -1,0 +1,71 @@
+"""CPU: the transaction model (SPEC acceptance 1, 2), the CLI's usage paths
+and the output writers (host formatting)."""
+
+import io
+
+import numpy as np
+import pytest
+
+from oracle import tiling as ot
+from paper_1611_02445_b200 import cli, geometry, layout, output, tiling, txmodel
+
+
+def test_acceptance1_transaction_arithmetic():
+    r = txmodel.count_tile_overheads(layout.LayoutTable.OPTIMIZED, "f64")
+    assert (r.tile_read_total, r.tile_read_min) == (344, 304)
+    assert abs(r.read_overhead - 0.1316) < 1e-3
+    assert r.per_direction_reads["NE"] == 20 and r.per_direction_reads["NW"] == 32
+    assert txmodel.count_tile_overheads(layout.LayoutTable.XYZ, "f32").tile_read_total == 288
+    assert txmodel.count_tile_overheads(layout.LayoutTable.OPTIMIZED, "f32").tile_read_total == 240
+    # the B200 table reaches the minimum when the tile is the request unit
+    assert txmodel.count_tile_reads_whole_tile(layout.LayoutTable.B200, "f64") == 304
+
+
+def test_acceptance2_cavity100_totals():
+    g = geometry.generate_cavity3d(100)
+    tm, ne = ot.build_tiling(g.types)
+    grid = tiling.TileGrid(4, g.shape, (100, 100, 100), tm, ne)
+    r = txmodel.geometry_transaction_totals(grid, g, layout.LayoutTable.OPTIMIZED, "f64")
+    assert (r.t_n, r.write_segments_min, r.nodetype_read_segments, r.total_min) == \
+        (15625, 4750000, 62500, 9562500)
+    assert r.tilemap_values_read == 421875
+
+
+def test_transaction_totals_match_reference(reference):
+    rx, rt, rg, rl = reference.txmodel, reference.tiling, reference.geometry, reference.layout
+    a = rg.generate_sphere_pack(32, 8, 0.6, seed=5)
+    ga = rt.build_tiling(a)
+    g = geometry.generate_sphere_pack(32, 8, 0.6, seed=5)
+    tm, ne = ot.build_tiling(g.types)
+    grid = tiling.TileGrid(4, g.shape, ga.padded_dims, tm, ne)
+    for t in ("optimized", "xyz"):
+        ra = rx.geometry_transaction_totals(ga, a, rl.LayoutTable(t), "f64")
+        rb = txmodel.geometry_transaction_totals(grid, g, layout.LayoutTable(t), "f64")
+        for k in ("write_segments_model", "read_segments_model", "total_model", "total_min"):
+            assert getattr(ra, k) == getattr(rb, k), k
+
+
+def test_cli_usage_and_count_tx(capsys):
+    assert cli.main(["count-tx", "--precision", "f32", "--layout", "xyz"]) == 0
+    assert "total,288" in capsys.readouterr().out
+    assert cli.main(["nope"]) == cli.EXIT_USAGE
+    with pytest.raises(cli.UsageError):
+        cli.parse_geometry("torus:3")
+
+
+def test_vtk_writer_format_and_determinism():
+    rng = np.random.default_rng(0)
+    rho = rng.random((3, 2, 4))
+    u = rng.random((3, 3, 2, 4))
+    a, b = io.StringIO(), io.StringIO()
+    output.write_vtk(a, rho, u)
+    output.write_vtk(b, rho, u)
+    text = a.getvalue()
+    assert text == b.getvalue()
+    lines = text.splitlines()
+    assert lines[0].startswith("# vtk DataFile") and "DIMENSIONS 3 2 4" in lines
+    assert "POINT_DATA 24" in lines
+    first = lines.index("LOOKUP_TABLE default") + 1
+    assert float(lines[first + 1]) == rho[1, 0, 0]          # x fastest
+    vec = lines.index("VECTORS velocity double") + 1
+    assert [float(v) for v in lines[vec].split()] == list(u[:, 0, 0, 0])
