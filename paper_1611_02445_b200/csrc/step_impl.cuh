@@ -70,6 +70,15 @@ constexpr int TILE_VALUES = Q * 64;
 template <class T>
 __device__ __forceinline__ T load_ro(const T *p) { return __ldg(p); }
 
+// Hide how a pointer was formed so the compiler keeps it as one 64-bit
+// register (base + 32-bit offset -> a single IMAD.WIDE per access) instead of
+// re-deriving src + tile * 1216 + offset for every load.
+template <class T>
+__device__ __forceinline__ const T *opaque(const T *p) {
+    asm("" : "+l"(p));
+    return p;
+}
+
 template <class T>
 __device__ __forceinline__ void store_out(T *p, T v) {
 #ifdef TLBM_STORE_CS
@@ -78,6 +87,37 @@ __device__ __forceinline__ void store_out(T *p, T v) {
     *p = v;
 #endif
 }
+
+// Pull table: for every (direction q, slot j) one packed word --
+//   bits  0-10  q*64 + L_q(source slot)        (pulled, in the source tile)
+//   bits 11-21  opp(q)*64 + L_opp(q)(j)        (halfway bounce-back, own tile)
+//   bits 22-26  neighbour-row index of the source tile delta (13 = own)
+// -- built at compile time per layout table (a __device__ constant), so
+// each pull costs one L1-resident table load instead of the per-direction
+// boundary tests and layout arithmetic.
+struct PullTable {
+    uint32_t w[Q * 64];
+};
+
+template <int TABLE>
+constexpr PullTable make_pull_table() {
+    PullTable t{};
+    for (int q = 0; q < Q; ++q)
+        for (int j = 0; j < 64; ++j) {
+            const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
+            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
+            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
+            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
+            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
+            const uint32_t pulled = q * 64 + layout_slot(kind_of(TABLE, q), sx & 3, sy & 3, sz & 3);
+            const uint32_t bounced = opp(q) * 64 + layout_slot(kind_of(TABLE, opp(q)), x, y, z);
+            t.w[q * 64 + j] = pulled | (bounced << 11) | ((uint32_t)delta_index(dx, dy, dz) << 22);
+        }
+    return t;
+}
+
+__device__ const PullTable kPullTables[3] = {make_pull_table<0>(), make_pull_table<1>(),
+                                             make_pull_table<2>()};
 
 // REL32: neighbour rows are staged as 32-bit element offsets relative to the
 // thread's own tile, so every per-direction address is one 32-bit add/select
@@ -98,6 +138,15 @@ step_kernel(const StepParams<T, MRT> p) {
     const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
     const long long tile = tile0 + ti;
 
+    // REL32 pulls read their packed word through the read-only path (the
+    // 4.9 KB table stays L1-resident).  Measured on B200 (scripts/step_sweep.py):
+    // fp32 0.50 ms vs 0.51-0.56 with per-direction address arithmetic and
+    // 0.57 with a per-CTA shared-memory copy (whose 640 MB/step of staging
+    // loads cost more than they save); fp64 unchanged at 0.78 ms.
+#ifndef TLBM_PULL_MODE
+#define TLBM_PULL_MODE 1   // 0: computed addresses, 1: packed pull table
+#endif
+    constexpr bool kTable = REL32 && VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE == 1;
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
             const long long t = tile0 + i / NBR;
@@ -112,12 +161,21 @@ step_kernel(const StepParams<T, MRT> p) {
     if (meta & META_ACTIVE) {
         const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
         const long long own = tile * TILE_VALUES;
-        const T *base = p.src + own;
+        const T *base = opaque(p.src + own);
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
+            if (VARIANT == TLBM_READ_WRITE_ONLY || (!kTable && q == 0)) {
                 g[q] = load_ro(base + (q * 64 + slot_of<TABLE>(q, x, y, z)));
+                continue;
+            }
+            if (kTable) {
+                // q = 0 needs no test: its word is (own slot, delta 13), and
+                // bit 0 of meta (the active bit) is set
+                const uint32_t w = __ldg(&kPullTables[TABLE].w[q * 64 + j]);
+                const int pulled = s_nbr[ti][w >> 22] + (int)(w & 0x7ffu);
+                const int bounced = (int)((w >> 11) & 0x7ffu);
+                g[q] = load_ro(base + (((meta >> q) & 1u) ? pulled : bounced));
                 continue;
             }
             const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
