@@ -1,0 +1,32 @@
+#!/bin/bash
+# Full evidence pass on the GPU box (via gpurun): bench line, launch list,
+# ncu --set full of the step kernel (fp64, fp32, MRT), sparse DRAM bytes,
+# porosity sweep, sanitizers.  Outputs under gpurun_out/$TAG/.
+set -u
+TAG=${1:-r1}
+O=gpurun_out/$TAG
+mkdir -p $O
+python bench.py > $O/bench.json 2> $O/bench.err
+python scripts/step_sweep.py --variants rw,prop,full,mrt > $O/ladder_f64.jsonl 2>/dev/null
+python scripts/step_sweep.py --variants rw,prop,full,mrt --precision f32 > $O/ladder_f32.jsonl 2>/dev/null
+python scripts/porosity_sweep.py --vessel --cavity > $O/sweep.jsonl 2> $O/sweep.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches.csv \
+    python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+for p in f64 f32; do
+  ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
+      -o $O/prof_step_$p python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --precision $p > /dev/null 2>&1
+done
+ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
+    -o $O/prof_step_mrt python scripts/step_sweep.py --variants mrt --steps 2 > /dev/null 2>&1
+for p in 0.2 0.5 0.9; do
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+      -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_p$p.csv \
+      python scripts/porosity_sweep.py --porosities $p --precisions f64 --steps 3 --warmup 5 > /dev/null 2>&1
+done
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_vessel.csv \
+    python scripts/porosity_sweep.py --porosities "" --vessel --precisions f64 --steps 3 --warmup 5 > /dev/null 2>&1
+timeout 900 compute-sanitizer --tool memcheck python scripts/sanitize_small.py > $O/memcheck.txt 2>&1
+timeout 900 compute-sanitizer --tool racecheck python scripts/sanitize_small.py > $O/racecheck.txt 2>&1
+tail -2 $O/memcheck.txt $O/racecheck.txt
+ls $O

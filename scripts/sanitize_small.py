@@ -18,6 +18,8 @@ for prec in ("f64", "f32"):
         s.step(1, variant=nat.READ_WRITE_ONLY)
         s.macroscopic()
         s.fields_canonical()
+s = solver.Solver(geo, solver.SimulationConfig(collision="mrt"))
+s.step(2)
 vs = slabs.VirtualSlabs(geometry.generate_channel("square", 12, axis=2, length=24,
                                                   ends="periodic"), 3)
 vs.step(3)
