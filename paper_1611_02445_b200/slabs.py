@@ -281,11 +281,25 @@ class IpcHalo:
         dist.all_gather_object(infos, info)
         self.bases = []
         mapped = {}
-        for nb in sorted({r.lower, r.upper} - {-1}):
-            store, b1 = _import(*infos[nb]["store"])
-            inbox, b2 = _import(*infos[nb]["inbox"])
-            mapped[nb] = (store, inbox)
-            self.bases += [b1, b2]
+        error = None
+        try:
+            for nb in sorted({r.lower, r.upper} - {-1}):
+                store, b1 = _import(*infos[nb]["store"])
+                self.bases.append(b1)
+                inbox, b2 = _import(*infos[nb]["inbox"])
+                self.bases.append(b2)
+                mapped[nb] = (store, inbox)
+        except RuntimeError as exc:           # e.g. no P2P path between the GPUs
+            error = exc
+        # every rank must take the same path (fused halo or fallback), or the
+        # collectives that follow would pair up wrongly and hang
+        oks = [None] * slab.plan.world
+        dist.all_gather_object(oks, error is None)
+        if not all(oks):
+            for b in self.bases:
+                nat.call("tlbm_ipc_close", nat.c_vp(b))
+            self.bases = []
+            raise RuntimeError(f"peer mapping failed on some rank ({error})")
         tv = 19 * 64 * self.esize
         self.up = None
         if r.upper >= 0:
