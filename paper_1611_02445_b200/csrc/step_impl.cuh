@@ -146,12 +146,16 @@ step_kernel(const StepParams<T, MRT> p) {
 #ifndef TLBM_PULL_MODE
 #define TLBM_PULL_MODE 1   // 0: computed addresses, 1: packed pull table
 #endif
-    constexpr bool kTable = REL32 && VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE == 1;
+    // The neighbour row is staged as the tile-index difference to the
+    // thread's own tile (0 for the own-tile entry 13); REL32 stores it
+    // pre-multiplied by the 1216 values of a tile.
+    constexpr bool kTable = VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE == 1;
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
             const long long t = tile0 + i / NBR;
             const long long nb = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
-            s_nbr[i / NBR][i % NBR] = (int)(REL32 ? (nb >= 0 ? (nb - t) * TILE_VALUES : 0) : nb);
+            const long long d = nb >= 0 ? nb - t : 0;
+            s_nbr[i / NBR][i % NBR] = (int)(REL32 ? d * TILE_VALUES : d);
         }
         __syncthreads();
     }
@@ -173,9 +177,16 @@ step_kernel(const StepParams<T, MRT> p) {
                 // q = 0 needs no test: its word is (own slot, delta 13), and
                 // bit 0 of meta (the active bit) is set
                 const uint32_t w = __ldg(&kPullTables[TABLE].w[q * 64 + j]);
-                const int pulled = s_nbr[ti][w >> 22] + (int)(w & 0x7ffu);
+                const int in_tile = (int)(w & 0x7ffu);
                 const int bounced = (int)((w >> 11) & 0x7ffu);
-                g[q] = load_ro(base + (((meta >> q) & 1u) ? pulled : bounced));
+                const bool link = (meta >> q) & 1u;
+                if (REL32) {
+                    const int pulled = s_nbr[ti][w >> 22] + in_tile;
+                    g[q] = load_ro(base + (link ? pulled : bounced));
+                } else {
+                    const long long rel = link ? (long long)s_nbr[ti][w >> 22] * TILE_VALUES : 0;
+                    g[q] = load_ro(base + rel + (link ? in_tile : bounced));
+                }
                 continue;
             }
             const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
@@ -185,14 +196,12 @@ step_kernel(const StepParams<T, MRT> p) {
             const int in_tile = q * 64 + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
             const int bounced = opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
             const bool link = (meta >> q) & 1u;
+            const int d = (dx | dy | dz) ? s_nbr[ti][delta_index(dx, dy, dz)] : 0;
             if (REL32) {
-                const int rel = (dx | dy | dz) ? s_nbr[ti][delta_index(dx, dy, dz)] : 0;
-                g[q] = load_ro(base + (link ? rel + in_tile : bounced));
+                g[q] = load_ro(base + (link ? d + in_tile : bounced));
             } else {
-                const long long nb = (dx | dy | dz) ? (long long)s_nbr[ti][delta_index(dx, dy, dz)]
-                                                    : tile;
-                const long long off = link ? nb * TILE_VALUES + in_tile : own + bounced;
-                g[q] = load_ro(p.src + off);
+                const long long rel = link ? (long long)d * TILE_VALUES : 0;
+                g[q] = load_ro(base + rel + (link ? in_tile : bounced));
             }
         }
 

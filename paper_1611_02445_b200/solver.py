@@ -99,7 +99,10 @@ class SimulationState:
 class Solver:
     """Device-resident tiled LBGK solver for one geometry on one GPU."""
 
-    def __init__(self, geometry, config=None, device=None, tiling=None):
+    def __init__(self, geometry, config=None, device=None, tiling=None, index64=False):
+        """``index64`` forces the step's 64-bit addressing path (used
+        automatically when neighbour offsets exceed 32 bits, i.e. beyond
+        ~1.76 M tiles); exposed for tests and measurements."""
         self.config = config if config is not None else SimulationConfig()
         self.geometry = geometry
         self.tiling = tiling if tiling is not None else DeviceTiling(geometry, device)
@@ -127,7 +130,7 @@ class Solver:
         a.inlet_u[:] = list(geometry.inlet_velocity)
         a.outlet_rho = float(geometry.outlet_density)
         a.u_guard = float(self.config.u_max_guard or 0.0)
-        a.rel32 = int(self.tiling.rel32)
+        a.rel32 = int(self.tiling.rel32 and not index64)
         self._mrt_op = self.config.mrt_operator        # kept alive for the ABI pointer
         if self._mrt_op is not None:
             self._mrt_op = np.ascontiguousarray(self._mrt_op)

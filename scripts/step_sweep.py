@@ -20,6 +20,7 @@ p.add_argument("--steps", type=int, default=100)
 p.add_argument("--variants", default="full,prop,rw")
 p.add_argument("--geometry", default="channel")
 p.add_argument("--porosity", type=float, default=0.5)
+p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
 a = p.parse_args()
 if a.geometry == "channel":
     geo = workloads.channel(a.n)
@@ -27,7 +28,8 @@ elif a.geometry == "cavity":
     geo = workloads.cavity(a.n)
 else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
-s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0))
+s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
+                          index64=a.index64)
 vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY,
         "mrt": nat.FULL}
 n_d = 8 if a.precision == "f64" else 4
@@ -39,7 +41,7 @@ for v in a.variants.split(","):
                                table=a.table, u_max_guard=0.0)
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
-        s = solvers["mrt"] = Solver(geo, cfg)
+        s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
     s.step(5, variant=vmap[v], check=False)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -50,7 +52,8 @@ for v in a.variants.split(","):
     ms = e0.elapsed_time(e1) / a.steps
     mlups = s.n_fn / (ms / 1e3) / 1e6
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
-    print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "geometry": a.geometry, "n": a.n,
+    print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
+                      "geometry": a.geometry, "n": a.n,
                       "precision": a.precision, "table": a.table, "variant": v,
                       "ms": round(ms, 4), "mlups": round(mlups, 1), "gbs": round(gbs, 1),
                       "frac": round(gbs / 6533.5, 4), "n_fn": s.n_fn, "t_n": s.t_n}), flush=True)

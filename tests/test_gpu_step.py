@@ -337,3 +337,23 @@ def test_mrt_sealed_box_mass_conservation(mn):
     m0 = s.total_mass()
     s.run(1000)
     assert abs(s.total_mass() - m0) / m0 <= 1e-10
+
+
+@pytest.mark.parametrize("coll", ["lbgk", "mrt"])
+def test_index64_path(c_oracle, coll):
+    """The 64-bit addressing variant (domains beyond ~1.76 M tiles) forced on a
+    small geometry: same bits as the oracle."""
+    geo = geometry.generate_sphere_pack(30, 8, 0.55, seed=21, inlet_velocity=(0, 0, 0.02))
+    for dt in (np.float64, np.float32):
+        for m in MODELS.values():
+            op = solver.SimulationConfig(collision="mrt").mrt_operator if coll == "mrt" else None
+            f0 = perturbed_eq(geo.shape, m, dt, (0.0, 0.0, 0.01), 7)
+            want = oracle_run(c_oracle, geo, m, dt, f0, 12, mrt_operator=op)
+            cfg = solver.SimulationConfig(collision=coll, fluid=m, tau=0.6, u_max_guard=0.0,
+                                          precision="f64" if dt == np.float64 else "f32",
+                                          mrt_matrix=op)
+            s = solver.Solver(geo, cfg, index64=True)
+            assert s._args.rel32 == 0
+            s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+            s.step(12)
+            compare(s, want, dt)
