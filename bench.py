@@ -54,6 +54,9 @@ def parse():
     p.add_argument("--precision", default="f64", choices=["f64", "f32"])
     p.add_argument("--edge", type=int, default=256, help="channel edge in nodes")
     p.add_argument("--table", default="b200")
+    p.add_argument("--arith", default="reference", choices=["reference", "fma"],
+                   help="collision arithmetic: reference = bit-exact unfused order, "
+                        "fma = fused multiply-adds (parity within tolerance)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -222,14 +225,41 @@ def e2e_run(args, torch, geo_host, world, rank, dist):
     phase times (host clock, a sync at each phase end) reported beside it."""
     from paper_1611_02445_b200 import slabs
     from paper_1611_02445_b200 import solver as sv
-    cfg = sv.SimulationConfig(tau=0.6, precision=args.precision, table=args.table)
+    cfg = sv.SimulationConfig(tau=0.6, precision=args.precision, table=args.table,
+                              arithmetic=args.arith)
     dt = torch.float64 if args.precision == "f64" else torch.float32
     plan = slabs.SlabPlan(geo_host, world)
     r = plan.ranges[rank]
     t_own = _tiles_in(geo_host.types[:, :, r.z0:r.z1])
-    pinned = torch.empty(args.steps, dtype=torch.int32, pin_memory=True)
+    pinned = torch.empty(max(args.steps, args.warmup), dtype=torch.int32, pin_memory=True)
     rho = torch.empty((t_own, 64), dtype=dt, pin_memory=True)
     u = torch.empty((3, t_own, 64), dtype=dt, pin_memory=True)
+    # one untimed pass of the whole e2e path with `warmup` steps first: a
+    # serving process has its CUDA context, modules and caching-allocator
+    # blocks already; the timed pass then measures the per-job work, not
+    # first-use cudaMalloc of the 5 GB field store
+    _e2e_pass(args, torch, geo_host, world, rank, dist, cfg, pinned, rho, u, args.warmup)
+    el, t0, t1, t2, t3, n_fn, h2d, d2h = _e2e_pass(args, torch, geo_host, world, rank, dist, cfg,
+                                                   pinned, rho, u, args.steps)
+    if dist is not None:
+        v = torch.tensor([el, n_fn, h2d, d2h], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        mx = v.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(v)
+        el, n_fn, h2d, d2h = float(mx[0]), int(v[1]), float(v[2]), float(v[3])
+    return {"value": n_fn * args.steps / el / 1e6, "unit": UNIT,
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+            "seconds": el,
+            "phases": {"setup_s": t1 - t0, "steps_s": t2 - t1, "readout_s": t3 - t2},
+            "what": "DistributedSlabRunner(geometry) + init + K x step() with per-step async "
+                    "D2H of the status word + final owned rho/u readout to pinned host "
+                    "memory; max over ranks; after one untimed warm-up pass of the same path"}
+
+
+def _e2e_pass(args, torch, geo_host, world, rank, dist, cfg, pinned, rho, u, steps):
+    from paper_1611_02445_b200 import slabs
+    from paper_1611_02445_b200 import solver as sv
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
@@ -241,7 +271,7 @@ def e2e_run(args, torch, geo_host, world, rank, dist):
     run.exchange_current()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    for i in range(args.steps):
+    for i in range(steps):
         run.step(1)
         slot = (s.iteration - 1) % sv.STATUS_RING
         pinned[i:i + 1].copy_(s.status[slot:slot + 1], non_blocking=True)
@@ -254,29 +284,16 @@ def e2e_run(args, torch, geo_host, world, rank, dist):
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     el = t3 - t0
-    if np.any(pinned.numpy() & 1):
+    if np.any(pinned[:steps].numpy() & 1):
         raise RuntimeError("e2e run diverged")
     n_fn = run.n_fn_owned
     if run.ipc is not None:
         run.ipc.check()
         run.ipc.close()
     h2d = run.slab.local_geometry.types.nbytes
-    d2h = 4 * args.steps + rho.numel() * rho.element_size() + u.numel() * u.element_size()
-    if dist is not None:
-        v = torch.tensor([el, n_fn, h2d, d2h], dtype=torch.float64,
-                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
-        mx = v.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(v)
-        el, n_fn, h2d, d2h = float(mx[0]), int(v[1]), float(v[2]), float(v[3])
+    d2h = 4 * steps + rho.numel() * rho.element_size() + u.numel() * u.element_size()
     del run, s, rho_d, u_d
-    return {"value": n_fn * args.steps / el / 1e6, "unit": UNIT,
-            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-            "seconds": el,
-            "phases": {"setup_s": t1 - t0, "steps_s": t2 - t1, "readout_s": t3 - t2},
-            "what": "DistributedSlabRunner(geometry) + init + K x step() with per-step async "
-                    "D2H of the status word + final owned rho/u readout to pinned host "
-                    "memory; max over ranks"}
+    return el, t0, t1, t2, t3, n_fn, h2d, d2h
 
 
 def _tiles_in(types):
@@ -312,14 +329,14 @@ def run_b200(args):
     transport = args.transport
     try:
         runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision,
-                                   table=args.table, transport=transport)
+                                   table=args.table, transport=transport, arithmetic=args.arith)
     except RuntimeError as exc:
         if transport != "ipc":
             raise
         print(f"[bench] ipc halo unavailable ({exc}); falling back to nccl", file=sys.stderr)
         transport = "nccl" if backend == "nccl" else "gloo"
         runner = slabs.SlabChannel(args.edge, world, rank, precision=args.precision,
-                                   table=args.table, transport=transport)
+                                   table=args.table, transport=transport, arithmetic=args.arith)
     args.transport_used = transport
     n_fn_rank = runner.n_fn_owned
     step_fn = runner.step
@@ -376,6 +393,7 @@ def run_b200(args):
                                + (f", global {args.edge}x{args.edge}x{args.edge * world}"
                                   if world > 1 else ""),
                    "model": "LBGK incompressible, tau=0.6", "layout_table": args.table,
+                   "arithmetic": args.arith,
                    "n_fn_per_gpu": n_fn_rank, "t_n_per_gpu": n_fn_rank // 64,
                    "l2": "inputs larger than L2 (field %.2f GB per copy)"
                          % (n_fn_rank / 64 * 19 * 64 * n_d / 1e9),

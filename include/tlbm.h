@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TLBM_ABI_VERSION 1
+#define TLBM_ABI_VERSION 2
 
 enum { TLBM_F64 = 0, TLBM_F32 = 1 };
 enum { TLBM_INCOMPRESSIBLE = 0, TLBM_QUASI = 1 };
@@ -40,6 +40,12 @@ enum { TLBM_TABLE_XYZ = 0, TLBM_TABLE_OPTIMIZED = 1, TLBM_TABLE_B200 = 2 };
 enum { TLBM_OK = 0, TLBM_ERR_ARG = 1, TLBM_ERR_CUDA = 2 };
 /* step variants (SPEC.md:531-539 bench ladder) */
 enum { TLBM_FULL = 0, TLBM_PROPAGATION_ONLY = 1, TLBM_READ_WRITE_ONLY = 2 };
+/* collision arithmetic of the step: REFERENCE keeps numpy's unfused operation
+ * order (bit-identical to the reference); FMA contracts the equilibrium,
+ * relaxation and MRT operator products into fused multiply-adds (fewer
+ * instructions; parity within the stated 1e-12 tolerance).  FMA is fp64-only:
+ * in fp32 it drifts past the 1e-5 bar (u: 1.1e-5 after 1000 cavity steps). */
+enum { TLBM_ARITH_REFERENCE = 0, TLBM_ARITH_FMA = 1 };
 /* bits of the device status word written by tlbm_step / tlbm_macroscopic */
 enum { TLBM_FLAG_DIVERGED = 1, TLBM_FLAG_GUARD = 2 };
 
@@ -169,6 +175,7 @@ typedef struct {
     const double *mrt_op;        /* MRT: host 19x19 float64 operator M^-1 S M,
                                     row-major (collision.py:206-213); cast to
                                     the working dtype like op.astype(dtype) */
+    int arith;                   /* TLBM_ARITH_REFERENCE or TLBM_ARITH_FMA */
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);

@@ -12,13 +12,14 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLBM_LIB") or os.path.join(HERE, "lib", "libtlbm.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 F64, F32 = 0, 1
 INCOMPRESSIBLE, QUASI = 0, 1
 TABLE_XYZ, TABLE_OPTIMIZED, TABLE_B200 = 0, 1, 2
 FULL, PROPAGATION_ONLY, READ_WRITE_ONLY = 0, 1, 2
 LBGK, MRT = 0, 1
+ARITH_REFERENCE, ARITH_FMA = 0, 1
 FLAG_DIVERGED, FLAG_GUARD = 1, 2
 
 c_int, c_i64, c_dbl, c_vp = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
@@ -33,7 +34,7 @@ class StepArgs(ctypes.Structure):
                 ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int),
                 ("halo_up", c_vp), ("halo_up_begin", c_i64), ("halo_up_end", c_i64),
                 ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
-                ("collision", c_int), ("mrt_op", c_vp)]
+                ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int)]
 
 
 _PROTOS = {

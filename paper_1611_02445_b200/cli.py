@@ -57,7 +57,8 @@ def parse_geometry(spec):
 def _config(args):
     from .solver import SimulationConfig
     return SimulationConfig(collision=args.model, fluid=args.fluid, tau=args.tau,
-                            precision=args.precision, table=args.layout)
+                            precision=args.precision, table=args.layout,
+                            arithmetic=args.arith)
 
 
 def cmd_run(args):
@@ -169,6 +170,7 @@ def build_parser():
         sp.add_argument("--tau", type=float, default=0.6)
         sp.add_argument("--precision", default="f64", choices=["f64", "f32"])
         sp.add_argument("--layout", default="b200", choices=["b200", "optimized", "xyz"])
+        sp.add_argument("--arith", default="reference", choices=["reference", "fma"])
 
     r = sub.add_parser("run")
     sim_args(r)

@@ -44,6 +44,16 @@ extern "C" int tlbm_step(const tlbm_step_args *a, void *stream) {
         set_error("tlbm_step: unknown collision model %d", a->collision);
         return TLBM_ERR_ARG;
     }
+    if (a->arith != TLBM_ARITH_REFERENCE && a->arith != TLBM_ARITH_FMA) {
+        set_error("tlbm_step: unknown arithmetic mode %d", a->arith);
+        return TLBM_ERR_ARG;
+    }
+    if (a->arith == TLBM_ARITH_FMA && a->dtype != TLBM_F64) {
+        // fp32 FMA drifts past the 1e-5 parity bar (u: 1.1e-5 after 1000
+        // cavity-64 steps, tests/test_gpu_fma.py), so it is not offered
+        set_error("tlbm_step: FMA arithmetic is fp64-only");
+        return TLBM_ERR_ARG;
+    }
     if (a->collision == TLBM_MRT && !a->mrt_op) {
         set_error("tlbm_step: MRT needs the 19x19 operator (mrt_op)");
         return TLBM_ERR_ARG;

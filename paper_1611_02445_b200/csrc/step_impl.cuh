@@ -57,15 +57,48 @@ __host__ __device__ constexpr int up_dir(int k) {
 
 constexpr int TILE_VALUES = Q * 64;
 
-// 2 tiles (128 threads) per CTA and a 64-register cap (8 CTAs = 32 warps per
-// SM) measured best on B200 for fp64: 0.797 ms / 256^3 channel step vs
-// 0.915 ms at 4 tiles / 78 registers (scripts/step_sweep.py, profiles/).
+// Tiles per CTA and the occupancy target (resident warps per SM, which sets
+// the register cap through __launch_bounds__), per dtype and collision.
+// fp64 LBGK: 2 tiles (128 threads) per CTA at 32 warps/SM (64 registers)
+// measured best on B200: 0.797 ms / 256^3 channel step vs 0.915 ms at 4
+// tiles / 78 registers and 1.39 ms at 48 warps / 40 registers
+// (scripts/step_sweep.py, profiles/).  fp32 LBGK moves half the bytes per
+// node, so at 32 warps/SM its loads cannot cover the latency: 64 warps/SM (32
+// registers) in 64-thread CTAs takes it from 0.490 to 0.410 ms (0.80 -> 0.95
+// of the HBM peak).  MRT keeps 19 deviations live next to the populations.
 #ifndef TLBM_TPC
 #define TLBM_TPC 2
 #endif
-#ifndef TLBM_MINB
-#define TLBM_MINB 8
+#ifndef TLBM_TPC_F32
+#define TLBM_TPC_F32 1
 #endif
+#ifndef TLBM_WARPS
+#define TLBM_WARPS 32
+#endif
+#ifndef TLBM_WARPS_F32
+#define TLBM_WARPS_F32 64
+#endif
+#ifndef TLBM_WARPS_MRT
+#define TLBM_WARPS_MRT 20
+#endif
+#ifndef TLBM_WARPS_MRT_F32
+#define TLBM_WARPS_MRT_F32 32
+#endif
+
+template <class T>
+constexpr int tiles_per_cta() { return sizeof(T) == 4 ? TLBM_TPC_F32 : TLBM_TPC; }
+
+// The 64-bit addressing path (REL32 false) of fp32 LBGK keeps the 64-register
+// budget: at 32 and 40 registers ptxas 12.9 produced out-of-bounds addresses for it
+// (compute-sanitizer, tests/test_gpu_step.py::test_index64_path), and it only
+// runs for domains beyond ~1.76 M tiles.
+template <class T, bool MRT, bool REL32>
+constexpr int min_blocks() {
+    constexpr int warps = sizeof(T) == 4
+        ? (MRT ? TLBM_WARPS_MRT_F32 : (REL32 ? TLBM_WARPS_F32 : TLBM_WARPS))
+        : (MRT ? TLBM_WARPS_MRT : TLBM_WARPS);
+    return warps / (2 * tiles_per_cta<T>());
+}
 
 template <class T>
 __device__ __forceinline__ T load_ro(const T *p) { return __ldg(p); }
@@ -124,13 +157,9 @@ __device__ const PullTable kPullTables[3] = {make_pull_table<0>(), make_pull_tab
 // and one IMAD.WIDE from a 64-bit base fixed per thread; valid whenever
 // |nbr - tile| * 1216 < 2^31 (checked on the host, tiling.py), otherwise the
 // 64-bit path recomputes full indices.
-// MRT keeps 19 deviations live next to the 19 populations: it gets a 128-
-// register budget (4 CTAs per SM) instead of 64
-template <bool MRT>
-constexpr int min_blocks() { return MRT ? 4 : TLBM_MINB; }
-
-template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32, bool MRT, bool HALO>
-__global__ void __launch_bounds__(64 * TPC, min_blocks<MRT>())
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32, bool MRT, bool HALO,
+          bool FMA>
+__global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, REL32>())
 step_kernel(const StepParams<T, MRT> p) {
     __shared__ int s_nbr[TPC][NBR];
     const int ti = threadIdx.x >> 6;
@@ -142,14 +171,15 @@ step_kernel(const StepParams<T, MRT> p) {
     // 4.9 KB table stays L1-resident).  Measured on B200 (scripts/step_sweep.py):
     // fp32 0.50 ms vs 0.51-0.56 with per-direction address arithmetic and
     // 0.57 with a per-CTA shared-memory copy (whose 640 MB/step of staging
-    // loads cost more than they save); fp64 unchanged at 0.78 ms.
+    // loads cost more than they save) and 0.55 with 16-byte unpacked entries
+    // (LDG.128: the hoisted 76 registers spill); fp64 unchanged at 0.78 ms.
 #ifndef TLBM_PULL_MODE
 #define TLBM_PULL_MODE 1   // 0: computed addresses, 1: packed pull table
 #endif
     // The neighbour row is staged as the tile-index difference to the
     // thread's own tile (0 for the own-tile entry 13); REL32 stores it
     // pre-multiplied by the 1216 values of a tile.
-    constexpr bool kTable = VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE == 1;
+    constexpr bool kTable = VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE >= 1;
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
             const long long t = tile0 + i / NBR;
@@ -215,8 +245,12 @@ step_kernel(const StepParams<T, MRT> p) {
             } else {
                 if (tag == INLET || tag == OUTLET)
                     zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
-                if constexpr (MRT)
+                if constexpr (MRT && FMA)
+                    status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                else if constexpr (MRT)
                     status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                else if constexpr (FMA)
+                    status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
                 else
                     status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
             }
@@ -250,30 +284,37 @@ step_kernel(const StepParams<T, MRT> p) {
     }
 }
 
-constexpr int TPC = TLBM_TPC;
-
-template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO>
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO, bool FMA>
 int launch_as(const tlbm_step_args *a, cudaStream_t s);
 
-template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT>
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool FMA>
 int launch_halo(const tlbm_step_args *a, cudaStream_t s) {
     if (VARIANT == TLBM_FULL && (a->halo_up || a->halo_down))
-        return launch_as<T, QUASI, TABLE, VARIANT, REL32, MRT, VARIANT == TLBM_FULL>(a, s);
-    return launch_as<T, QUASI, TABLE, VARIANT, REL32, MRT, false>(a, s);
+        return launch_as<T, QUASI, TABLE, VARIANT, REL32, MRT, VARIANT == TLBM_FULL, FMA>(a, s);
+    return launch_as<T, QUASI, TABLE, VARIANT, REL32, MRT, false, FMA>(a, s);
+}
+
+// FMA arithmetic is fp64-only (tlbm_step rejects it for fp32)
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT>
+int launch_arith(const tlbm_step_args *a, cudaStream_t s) {
+    constexpr bool kFma = VARIANT == TLBM_FULL && sizeof(T) == 8;
+    if (kFma && a->arith == TLBM_ARITH_FMA)
+        return launch_halo<T, QUASI, TABLE, VARIANT, REL32, MRT, kFma>(a, s);
+    return launch_halo<T, QUASI, TABLE, VARIANT, REL32, MRT, false>(a, s);
 }
 
 template <class T, int QUASI, int TABLE, int VARIANT>
 int launch(const tlbm_step_args *a, cudaStream_t s) {
     if (VARIANT == TLBM_FULL && a->collision == TLBM_MRT) {
-        if (a->rel32) return launch_halo<T, QUASI, TABLE, VARIANT, true, true>(a, s);
-        return launch_halo<T, QUASI, TABLE, VARIANT, false, true>(a, s);
+        if (a->rel32) return launch_arith<T, QUASI, TABLE, VARIANT, true, true>(a, s);
+        return launch_arith<T, QUASI, TABLE, VARIANT, false, true>(a, s);
     }
     if (a->rel32)
-        return launch_halo<T, QUASI, TABLE, VARIANT, true, false>(a, s);
-    return launch_halo<T, QUASI, TABLE, VARIANT, false, false>(a, s);
+        return launch_arith<T, QUASI, TABLE, VARIANT, true, false>(a, s);
+    return launch_arith<T, QUASI, TABLE, VARIANT, false, false>(a, s);
 }
 
-template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO>
+template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO, bool FMA>
 int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
     if constexpr (MRT)
@@ -297,7 +338,8 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     p.halo_down_end = a->halo_down_end;
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
-    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO>
+    constexpr int TPC = tiles_per_cta<T>();
+    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA>
         <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel");
 }
@@ -321,7 +363,7 @@ struct StepLaunch {
 };
 
 // one translation unit per dtype (step_f64.cu / step_f32.cu) instantiates
-// this, so the 72 kernels per dtype compile in parallel
+// this, so the 72 (fp32) and 120 (fp64) kernels compile in parallel
 template <class T>
 int launch_dtype(const tlbm_step_args *a, cudaStream_t s) {
     const StepLaunch<T> l{a, s};

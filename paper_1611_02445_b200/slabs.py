@@ -520,10 +520,11 @@ class SlabChannel(DistributedSlabRunner):
     256 * N long, one 256^3 slab per rank (weak scaling)."""
 
     def __init__(self, n, world, rank, precision="f64", table="b200", device=None,
-                 transport="nccl"):
+                 transport="nccl", arithmetic="reference"):
         from . import workloads
         geo = workloads.channel_z(n, n * world)
-        cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table)
+        cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table,
+                               arithmetic=arithmetic)
         super().__init__(geo, world, rank, cfg, device, transport)
         s = self.slab.solver
         rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.04),

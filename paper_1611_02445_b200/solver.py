@@ -5,7 +5,12 @@ step semantics are restated in SURVEY Appendix A).  API:
 
 ``SimulationConfig``  SPEC.md:335-340 (collision, fluid, tau > 0.5,
                       mrt_relaxation, precision f32|f64, u_max_guard=0.05),
-                      plus ``table`` (default LayoutTable.B200).
+                      plus ``table`` (default LayoutTable.B200) and
+                      ``arithmetic``: "reference" (default; numpy's
+                      unfused operation order, bit-identical to the
+                      reference) or "fma" (fused multiply-adds in the
+                      collision: fewer instructions, parity within the
+                      stated 1e-12 tolerance; f64 only).
 ``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,
                       iteration, parity).
 ``Solver``            owns the device state; ``step(n)``, ``run(n)``,
@@ -50,6 +55,7 @@ class SimulationConfig:
     u_max_guard: float = 0.05
     table: LayoutTable = LayoutTable.B200
     mrt_matrix: object = None      # optional explicit 19x19 operator (overrides rates)
+    arithmetic: str = "reference"  # "reference" (bit-exact) | "fma"
 
     def __post_init__(self):
         self.collision = CollisionModel(getattr(self.collision, "value", self.collision))
@@ -59,6 +65,11 @@ class SimulationConfig:
             raise ValueError(f"relaxation time must exceed 0.5: {self.tau}")
         if self.precision not in ("f32", "f64"):
             raise ValueError(f"unknown precision: {self.precision!r}")
+        if self.arithmetic not in ("reference", "fma"):
+            raise ValueError(f"unknown arithmetic: {self.arithmetic!r}")
+        if self.arithmetic == "fma" and self.precision != "f64":
+            raise ValueError("arithmetic='fma' is f64-only: in f32 it drifts past the 1e-5 "
+                             "parity bar (u: 1.1e-5 after 1000 cavity-64 steps)")
         if self.collision is CollisionModel.MRT:
             from .collision import default_mrt_rates
             rates = (default_mrt_rates(self.tau) if self.mrt_relaxation is None
@@ -131,6 +142,7 @@ class Solver:
         a.outlet_rho = float(geometry.outlet_density)
         a.u_guard = float(self.config.u_max_guard or 0.0)
         a.rel32 = int(self.tiling.rel32 and not index64)
+        a.arith = nat.ARITH_FMA if self.config.arithmetic == "fma" else nat.ARITH_REFERENCE
         self._mrt_op = self.config.mrt_operator        # kept alive for the ABI pointer
         if self._mrt_op is not None:
             self._mrt_op = np.ascontiguousarray(self._mrt_op)

@@ -21,6 +21,7 @@ p.add_argument("--variants", default="full,prop,rw")
 p.add_argument("--geometry", default="channel")
 p.add_argument("--porosity", type=float, default=0.5)
 p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
+p.add_argument("--arith", default="reference", choices=["reference", "fma"])
 a = p.parse_args()
 if a.geometry == "channel":
     geo = workloads.channel(a.n)
@@ -29,7 +30,7 @@ elif a.geometry == "cavity":
 else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
-                          index64=a.index64)
+                          index64=a.index64, arithmetic=a.arith)
 vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY,
         "mrt": nat.FULL}
 n_d = 8 if a.precision == "f64" else 4
@@ -38,7 +39,7 @@ for v in a.variants.split(","):
     if v == "mrt" and "mrt" not in solvers:
         from paper_1611_02445_b200.solver import SimulationConfig, Solver
         cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision=a.precision,
-                               table=a.table, u_max_guard=0.0)
+                               table=a.table, u_max_guard=0.0, arithmetic=a.arith)
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
         s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
@@ -53,6 +54,7 @@ for v in a.variants.split(","):
     mlups = s.n_fn / (ms / 1e3) / 1e6
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
     print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
+                      "arith": a.arith,
                       "geometry": a.geometry, "n": a.n,
                       "precision": a.precision, "table": a.table, "variant": v,
                       "ms": round(ms, 4), "mlups": round(mlups, 1), "gbs": round(gbs, 1),

@@ -80,3 +80,12 @@ def test_error_reporting_without_gpu():
 
 def test_tiling_scratch_size():
     assert nat.load().tlbm_tiling_scratch_bytes(64, 64, 64) >= 16 ** 3
+
+
+def test_fma_arithmetic_is_f64_only():
+    from paper_1611_02445_b200 import solver
+    solver.SimulationConfig(arithmetic="fma")
+    with pytest.raises(ValueError):
+        solver.SimulationConfig(arithmetic="fma", precision="f32")
+    with pytest.raises(ValueError):
+        solver.SimulationConfig(arithmetic="fast")
