@@ -176,9 +176,20 @@ typedef struct {
                                     row-major (collision.py:206-213); cast to
                                     the working dtype like op.astype(dtype) */
     int arith;                   /* TLBM_ARITH_REFERENCE or TLBM_ARITH_FMA */
+    /* graph-replayable status ring (may be NULL): when set, `flags` is the
+     * base of a ring of ring_len words and the launch ORs its status into
+     * flags[(*iter_counter + iter_add) % ring_len], the iteration number read
+     * on the device (only by warps that have a status bit to report), so one
+     * captured CUDA graph of K steps can be replayed with
+     * tlbm_advance_counter(iter_counter, K) as its last node. */
+    const int64_t *iter_counter;
+    int64_t iter_add;
+    int ring_len;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);
+/* *d_counter += k (one thread; the last node of a captured step graph). */
+int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream);
 
 /* ---- peer memory for the fused halo (csrc/peer.cu) ---------------------- */
 /* CUDA IPC export of a device pointer: 64-byte handle + offset of d_ptr in

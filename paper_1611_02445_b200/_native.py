@@ -34,7 +34,8 @@ class StepArgs(ctypes.Structure):
                 ("u_guard", c_dbl), ("flags", c_vp), ("rel32", c_int),
                 ("halo_up", c_vp), ("halo_up_begin", c_i64), ("halo_up_end", c_i64),
                 ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
-                ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int)]
+                ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int),
+                ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int)]
 
 
 _PROTOS = {
@@ -70,6 +71,7 @@ _PROTOS = {
                             c_dbl, c_dbl, c_vp, c_vp]),
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
+    "tlbm_advance_counter": (c_int, [c_vp, c_i64, c_vp]),
     "tlbm_ipc_export": (c_int, [c_vp, c_vp, ctypes.POINTER(ctypes.c_uint64)]),
     "tlbm_ipc_import": (c_int, [c_vp, ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "tlbm_ipc_close": (c_int, [c_vp]),

@@ -62,10 +62,28 @@ extern "C" int tlbm_step(const tlbm_step_args *a, void *stream) {
         set_error("tlbm_step: relaxation time must exceed 0.5, got %g", a->tau);
         return TLBM_ERR_ARG;
     }
+    if (a->iter_counter && (!a->flags || a->ring_len <= 0)) {
+        set_error("tlbm_step: a device iteration counter needs flags and ring_len > 0");
+        return TLBM_ERR_ARG;
+    }
     int rc;
     if ((rc = check_dtype(a->dtype)) || (rc = check_fluid(a->fluid)) ||
         (rc = check_table(a->table)))
         return rc;
     return a->dtype == TLBM_F64 ? step_launch_f64(a, as_stream(stream))
                                 : step_launch_f32(a, as_stream(stream));
+}
+
+namespace {
+__global__ void advance_counter_kernel(long long *c, long long k) { *c += k; }
+}  // namespace
+
+extern "C" int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream) {
+    if (!d_counter) {
+        set_error("tlbm_advance_counter: null counter");
+        return TLBM_ERR_ARG;
+    }
+    advance_counter_kernel<<<1, 1, 0, as_stream(stream)>>>(
+        reinterpret_cast<long long *>(d_counter), (long long)k);
+    return launch_check("advance_counter_kernel");
 }

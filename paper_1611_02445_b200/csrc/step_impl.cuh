@@ -43,6 +43,9 @@ struct StepParams {
     double outlet_rho;
     double guard_sq;        // |u|^2 threshold of the guard (+inf: off)
     uint32_t *flags;
+    const long long *iter;  // graph mode: status ring slot read on the device
+    long long iter_add;
+    unsigned long long ring_len;
     // fused halo: post-collision outgoing z planes also stored into a
     // neighbour's ghost tiles (peer memory), tile t -> dst + (t - begin) * 1216
     T *halo_up;             // e_z = +1 directions of plane z = 3
@@ -88,14 +91,19 @@ constexpr int TILE_VALUES = Q * 64;
 template <class T>
 constexpr int tiles_per_cta() { return sizeof(T) == 4 ? TLBM_TPC_F32 : TLBM_TPC; }
 
-// The 64-bit addressing path (REL32 false) of fp32 LBGK keeps the 64-register
-// budget: at 32 and 40 registers ptxas 12.9 produced out-of-bounds addresses for it
-// (compute-sanitizer, tests/test_gpu_step.py::test_index64_path), and it only
-// runs for domains beyond ~1.76 M tiles.
-template <class T, bool MRT, bool REL32>
+// (The 64-bit path's earlier formulation -- 64-bit offsets rebuilt per pull --
+// came out of ptxas 12.9 with out-of-bounds addresses at 32 and 40 registers
+// (compute-sanitizer, tests/test_gpu_step.py::test_index64_path); the staged
+// block pointers below are clean at 32 and run 0.89 of peak in fp32.)
+// fp32 propagation-only (bench ladder): 48 warps/SM, 0.416 ms vs 0.441 at 64
+#ifndef TLBM_WARPS_PROP_F32
+#define TLBM_WARPS_PROP_F32 48
+#endif
+template <class T, bool MRT, int VARIANT>
 constexpr int min_blocks() {
     constexpr int warps = sizeof(T) == 4
-        ? (MRT ? TLBM_WARPS_MRT_F32 : (REL32 ? TLBM_WARPS_F32 : TLBM_WARPS))
+        ? (MRT ? TLBM_WARPS_MRT_F32
+               : (VARIANT == TLBM_PROPAGATION_ONLY ? TLBM_WARPS_PROP_F32 : TLBM_WARPS_F32))
         : (MRT ? TLBM_WARPS_MRT : TLBM_WARPS);
     return warps / (2 * tiles_per_cta<T>());
 }
@@ -155,13 +163,15 @@ __device__ const PullTable kPullTables[3] = {make_pull_table<0>(), make_pull_tab
 // REL32: neighbour rows are staged as 32-bit element offsets relative to the
 // thread's own tile, so every per-direction address is one 32-bit add/select
 // and one IMAD.WIDE from a 64-bit base fixed per thread; valid whenever
-// |nbr - tile| * 1216 < 2^31 (checked on the host, tiling.py), otherwise the
-// 64-bit path recomputes full indices.
+// |nbr - tile| * 1216 < 2^31 (checked on the host, tiling.py).  Otherwise
+// (e.g. a periodic wrap across more than 1.77 M tiles) the 64-bit path stages
+// the 27 neighbour block addresses themselves and selects a pointer per pull.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32, bool MRT, bool HALO,
           bool FMA>
-__global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, REL32>())
+__global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, VARIANT>())
 step_kernel(const StepParams<T, MRT> p) {
     __shared__ int s_nbr[TPC][NBR];
+    __shared__ const T *s_ptr[REL32 ? 1 : TPC][NBR];
     const int ti = threadIdx.x >> 6;
     const int j = threadIdx.x & 63;
     const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
@@ -186,6 +196,7 @@ step_kernel(const StepParams<T, MRT> p) {
             const long long nb = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
             const long long d = nb >= 0 ? nb - t : 0;
             s_nbr[i / NBR][i % NBR] = (int)(REL32 ? d * TILE_VALUES : d);
+            if (!REL32) s_ptr[REL32 ? 0 : i / NBR][i % NBR] = p.src + (t + d) * TILE_VALUES;
         }
         __syncthreads();
     }
@@ -214,8 +225,8 @@ step_kernel(const StepParams<T, MRT> p) {
                     const int pulled = s_nbr[ti][w >> 22] + in_tile;
                     g[q] = load_ro(base + (link ? pulled : bounced));
                 } else {
-                    const long long rel = link ? (long long)s_nbr[ti][w >> 22] * TILE_VALUES : 0;
-                    g[q] = load_ro(base + rel + (link ? in_tile : bounced));
+                    const T *src = link ? s_ptr[REL32 ? 0 : ti][w >> 22] : base;
+                    g[q] = load_ro(src + (link ? in_tile : bounced));
                 }
                 continue;
             }
@@ -278,9 +289,12 @@ step_kernel(const StepParams<T, MRT> p) {
         // one atomic per warp, and only for bits not yet set: a flow sitting at
         // the |u| guard must not serialise every warp on one L2 address
         const uint32_t any = __reduce_or_sync(0xffffffffu, status);
-        if (any && (threadIdx.x & 31) == 0 &&
-            (any & ~*reinterpret_cast<volatile uint32_t *>(p.flags)))
-            atomicOr(p.flags, any);
+        if (any && (threadIdx.x & 31) == 0) {
+            uint32_t *f = p.flags;
+            if (p.iter)
+                f += (unsigned long long)(*p.iter + p.iter_add) % p.ring_len;
+            if (any & ~*reinterpret_cast<volatile uint32_t *>(f)) atomicOr(f, any);
+        }
     }
 }
 
@@ -330,6 +344,9 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     p.outlet_rho = a->outlet_rho;
     p.guard_sq = a->u_guard > 0.0 ? a->u_guard * a->u_guard : HUGE_VAL;
     p.flags = a->flags;
+    p.iter = reinterpret_cast<const long long *>(a->iter_counter);
+    p.iter_add = a->iter_add;
+    p.ring_len = (unsigned long long)(a->ring_len > 0 ? a->ring_len : 1);
     p.halo_up = static_cast<T *>(a->halo_up);
     p.halo_up_begin = a->halo_up_begin;
     p.halo_up_end = a->halo_up_end;

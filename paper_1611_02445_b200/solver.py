@@ -39,6 +39,7 @@ from .lattice import Q, WEIGHTS
 from .tiling import DeviceTiling
 
 STATUS_RING = 4096
+GRAPH_STEPS = 64      # steps per captured CUDA graph (even: the parity is restored)
 
 
 class CompressibilityWarning(UserWarning):
@@ -151,6 +152,9 @@ class Solver:
         else:
             a.collision = nat.LBGK
         self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
+        self._graphs = {}
+        self._iter_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._iter_dev_value = 0
         self.init_equilibrium()
 
     # -- initial state -------------------------------------------------------
@@ -192,17 +196,28 @@ class Solver:
         self.status.zero_()
 
     # -- stepping ------------------------------------------------------------
-    def step(self, n=1, variant=nat.FULL, check=True):
+    def step(self, n=1, variant=nat.FULL, check=True, graph=False):
         """Advance n iterations (no host sync unless ``check`` and the status
-        ring is full or n is exhausted)."""
+        ring is full or n is exhausted).  ``graph``: run whole blocks of
+        GRAPH_STEPS iterations as replays of a captured CUDA graph (one
+        launch per block instead of one ctypes call per step; for small
+        domains whose step takes a few microseconds)."""
         nat.require_cuda(self.device)
+        n = int(n)
+        if graph:
+            while n >= GRAPH_STEPS:
+                if self.iteration + GRAPH_STEPS - self._checked > STATUS_RING:
+                    self.check()
+                self._replay(int(variant))
+                n -= GRAPH_STEPS
         a = self._args
         a.variant = int(variant)
         a.tile_begin, a.tile_end = 0, self.t_n
+        a.iter_counter = None
         stream = nat.stream_ptr(self.device)
         lib = nat.load()
         base = self.status.data_ptr()
-        for _ in range(int(n)):
+        for _ in range(n):
             if self.iteration - self._checked >= STATUS_RING:
                 self.check()
             a.f_src = self._copies[self.parity]
@@ -216,6 +231,46 @@ class Solver:
         if check:
             self.check()
         return self
+
+    def _replay(self, variant):
+        """GRAPH_STEPS iterations as one CUDA graph replay.  The graph holds
+        GRAPH_STEPS step launches (copies alternating from the current
+        parity, status slot (device iteration counter + i) % STATUS_RING)
+        and a last node advancing the device counter, so it replays without
+        host-side parameter updates."""
+        key = (self.parity, variant)
+        g = self._graphs.get(key)
+        if g is None:
+            g = self._capture(variant)
+            self._graphs[key] = g
+        if self._iter_dev_value != self.iteration:
+            self._iter_dev.fill_(self.iteration)
+        g.replay()
+        self.iteration += GRAPH_STEPS
+        self._iter_dev_value = self.iteration
+
+    def _capture(self, variant):
+        a = nat.StepArgs()
+        ctypes_copy = nat.ctypes.pointer(a)
+        nat.ctypes.memmove(ctypes_copy, nat.ctypes.byref(self._args), nat.ctypes.sizeof(a))
+        a.variant = variant
+        a.tile_begin, a.tile_end = 0, self.t_n
+        a.flags = self.status.data_ptr()
+        a.iter_counter = self._iter_dev.data_ptr()
+        a.ring_len = STATUS_RING
+        lib = nat.load()
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize(self.device)
+        with torch.cuda.device(self.device), torch.cuda.graph(g):
+            stream = nat.stream_ptr(self.device)
+            par = self.parity
+            for i in range(GRAPH_STEPS):
+                a.f_src, a.f_dst = self._copies[par], self._copies[1 - par]
+                a.iter_add = i
+                nat.check(lib.tlbm_step(nat.ctypes.byref(a), stream))
+                par ^= 1
+            nat.check(lib.tlbm_advance_counter(nat.ptr(self._iter_dev), GRAPH_STEPS, stream))
+        return g
 
     def check(self):
         """Read the status ring; raise DivergenceError at the first divergent
@@ -240,11 +295,11 @@ class Solver:
                           f"{self.guard_iterations[-1]}", CompressibilityWarning, stacklevel=2)
         self._checked = self.iteration
 
-    def run(self, iterations, check_every=STATUS_RING):
+    def run(self, iterations, check_every=STATUS_RING, graph=False):
         left = int(iterations)
         while left > 0:
             k = min(left, check_every)
-            self.step(k, check=True)
+            self.step(k, check=True, graph=graph)
             left -= k
         return self
 

@@ -4,7 +4,7 @@
 
 Reads `ncu -i --page raw --csv`; reports duration, DRAM bytes (read/write)
 per launch, throughput, L1/L2 sector counts and hit rates, occupancy and
-registers -- and, given n_fn, DRAM bytes per fluid node vs the 304 B model.
+registers -- and, given n_fn, DRAM bytes per fluid node vs the 304 B (fp64) / 152 B (fp32) model.
 """
 import csv
 import io
@@ -62,7 +62,7 @@ def main():
                 rec["dram_gbs"] = rec["dram_bytes"] / rec["duration"] / 1e9
             if n_fn:
                 rec["dram_bytes_per_node"] = rec["dram_bytes"] / n_fn
-                rec["algorithmic_bytes_per_node"] = 304
+                rec["algorithmic_bytes_per_node"] = 152 if "<float" in rec.get("kernel", "") else 304
         out.append(rec)
     json.dump(out, sys.stdout, indent=1)
     print()

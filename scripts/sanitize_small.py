@@ -18,8 +18,14 @@ for prec in ("f64", "f32"):
         s.step(1, variant=nat.READ_WRITE_ONLY)
         s.macroscopic()
         s.fields_canonical()
-s = solver.Solver(geo, solver.SimulationConfig(collision="mrt"))
-s.step(2)
+for coll in ("lbgk", "mrt"):
+    for prec in ("f64", "f32"):
+        s = solver.Solver(geo, solver.SimulationConfig(collision=coll, precision=prec))
+        s.step(2)
+        s = solver.Solver(geo, solver.SimulationConfig(collision=coll, precision=prec), index64=True)
+        s.step(2)
+    s = solver.Solver(geo, solver.SimulationConfig(collision=coll, arithmetic="fma"))
+    s.step(2)
 vs = slabs.VirtualSlabs(geometry.generate_channel("square", 12, axis=2, length=24,
                                                   ends="periodic"), 3)
 vs.step(3)

@@ -18,19 +18,28 @@ p.add_argument("--precision", default="f64")
 p.add_argument("--table", default="b200")
 p.add_argument("--steps", type=int, default=100)
 p.add_argument("--variants", default="full,prop,rw")
-p.add_argument("--geometry", default="channel")
+p.add_argument("--geometry", default="channel", help="channel | channel_z | cavity | pack")
+p.add_argument("--length", type=int, default=None, help="channel_z length along z")
+p.add_argument("--no-perturb", action="store_true",
+               help="uniform equilibrium start (no (t_n, 64) init temporaries; big domains)")
 p.add_argument("--porosity", type=float, default=0.5)
 p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
 p.add_argument("--arith", default="reference", choices=["reference", "fma"])
+p.add_argument("--graph", action="store_true", help="replay captured CUDA graphs of steps")
 a = p.parse_args()
 if a.geometry == "channel":
     geo = workloads.channel(a.n)
+elif a.geometry == "channel_z":
+    geo = workloads.channel_z(a.n, a.length)
 elif a.geometry == "cavity":
     geo = workloads.cavity(a.n)
 else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
-                          index64=a.index64, arithmetic=a.arith)
+                          index64=a.index64, arithmetic=a.arith, perturb=not a.no_perturb)
+if a.no_perturb:
+    s.init_equilibrium(1.0, (0.0, 0.0, 0.04) if a.geometry == "channel_z" else (0.04, 0.0, 0.0))
+from paper_1611_02445_b200.solver import GRAPH_STEPS as solver_graph_steps  # noqa: E402
 vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY,
         "mrt": nat.FULL}
 n_d = 8 if a.precision == "f64" else 4
@@ -43,19 +52,20 @@ for v in a.variants.split(","):
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
         s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
-    s.step(5, variant=vmap[v], check=False)
+    s.step(solver_graph_steps if a.graph else 5, variant=vmap[v], check=False, graph=a.graph)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    s.step(a.steps, variant=vmap[v], check=False)
+    s.step(a.steps, variant=vmap[v], check=False, graph=a.graph)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     mlups = s.n_fn / (ms / 1e3) / 1e6
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
     print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
-                      "arith": a.arith,
-                      "geometry": a.geometry, "n": a.n,
+                      "arith": a.arith, "graph": a.graph,
+                      "geometry": a.geometry, "n": a.n, "dims": list(geo.shape),
+                      "field_gb": round(2 * s.t_n * 19 * 64 * n_d / 1e9, 2),
                       "precision": a.precision, "table": a.table, "variant": v,
                       "ms": round(ms, 4), "mlups": round(mlups, 1), "gbs": round(gbs, 1),
                       "frac": round(gbs / 6533.5, 4), "n_fn": s.n_fn, "t_n": s.t_n}), flush=True)
