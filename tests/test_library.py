@@ -89,3 +89,22 @@ def test_fma_arithmetic_is_f64_only():
         solver.SimulationConfig(arithmetic="fma", precision="f32")
     with pytest.raises(ValueError):
         solver.SimulationConfig(arithmetic="fast")
+
+
+def test_step_args_layout_matches_header(tmp_path):
+    """ctypes StepArgs (_native.py) has the field offsets and size of the C
+    tlbm_step_args in include/tlbm.h (compiled here with gcc)."""
+    import ctypes
+    import subprocess
+    names = [f[0] for f in nat.StepArgs._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stdio.h>\n#include <stddef.h>\n#include \"tlbm.h\"\nint main(void){\n"
+                   + "".join(f'printf("%zu\\n", offsetof(tlbm_step_args, {n}));\n' for n in names)
+                   + 'printf("%zu\\n", sizeof(tlbm_step_args));\nreturn 0;}\n')
+    exe = tmp_path / "layout"
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [getattr(nat.StepArgs, n).offset for n in names] + [ctypes.sizeof(nat.StepArgs)]
+    assert got == want
