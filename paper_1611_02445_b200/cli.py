@@ -64,9 +64,10 @@ def _config(args):
 def cmd_run(args):
     from . import solver
     geo = parse_geometry(args.geometry)
-    outputs = {"vtk": args.vtk, "csv": args.csv,
+    outputs = {"vtk": args.vtk, "csv": args.csv, "checkpoint": args.checkpoint,
                "convergence_every": args.convergence_every, "tolerance": args.tolerance}
-    _, diag = solver.run(_config(args), geo, args.iters, outputs=outputs)
+    _, diag = solver.run(_config(args), geo, args.iters, outputs=outputs,
+                         resume_from=args.resume, graph=args.graph)
     print(json.dumps(diag))
     return EXIT_OK
 
@@ -179,6 +180,9 @@ def build_parser():
     r.add_argument("--csv")
     r.add_argument("--convergence-every", type=int, default=0)
     r.add_argument("--tolerance", type=float)
+    r.add_argument("--checkpoint", help="save the final state here (.npz)")
+    r.add_argument("--resume", help="start from this checkpoint (same geometry)")
+    r.add_argument("--graph", action="store_true", help="replay CUDA graphs of 64 steps")
     b = sub.add_parser("bench")
     sim_args(b)
     b.add_argument("--variant", default="full", choices=["full", "prop", "rw"])

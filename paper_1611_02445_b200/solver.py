@@ -25,6 +25,8 @@ into a per-iteration status word of a ring buffer; ``check()`` reads it and
 raises ``DivergenceError`` with the exact iteration.
 """
 
+import hashlib
+import json
 import warnings
 from dataclasses import dataclass, field
 
@@ -359,6 +361,43 @@ class Solver:
         nx, ny, nz = self.tiling.dims
         return out[..., :nx, :ny, :nz]
 
+    # -- checkpoint / resume --------------------------------------------------
+    def save_checkpoint(self, path):
+        """Write the current state to ``path`` (.npz): the canonical
+        (19, t_n, 64) populations of the current copy in the working dtype,
+        the iteration, the configuration and a fingerprint of the geometry.
+        Only the current copy is state: the next step rewrites every active
+        slot of the other one, and solid slots are never read."""
+        self.check()
+        cfg = {k: (v.value if hasattr(v, "value") else v)
+               for k, v in self.config.__dict__.items() if k != "mrt_matrix"}
+        extra = {}
+        if self.config.mrt_matrix is not None:
+            extra["mrt_matrix"] = np.asarray(self.config.mrt_matrix, dtype=np.float64)
+        np.savez(path, format=np.array(CHECKPOINT_FORMAT), f=self.fields_canonical(),
+                 iteration=np.int64(self.iteration), config=np.array(json.dumps(cfg)),
+                 geometry=np.array(geometry_fingerprint(self.geometry)), **extra)
+
+    def load_checkpoint(self, path):
+        """Restore a state written by save_checkpoint into this solver (same
+        geometry and precision); stepping on is bit-identical to never having
+        stopped."""
+        with np.load(path, allow_pickle=False) as z:
+            if str(z["format"]) != CHECKPOINT_FORMAT:
+                raise ValueError(f"{path}: not a {CHECKPOINT_FORMAT} checkpoint")
+            if str(z["geometry"]) != geometry_fingerprint(self.geometry):
+                raise ValueError(f"{path}: checkpoint was written for another geometry")
+            f = z["f"]
+            if f.dtype != self.config.dtype or f.shape != (Q, self.t_n, 64):
+                raise ValueError(f"{path}: fields {f.dtype} {f.shape} do not fit this solver "
+                                 f"({np.dtype(self.config.dtype)}, t_n {self.t_n})")
+            it = int(z["iteration"])
+        self._reset_counters()
+        self.iteration = self._checked = it
+        self.parity = it & 1
+        self.store.fill_canonical(self.parity, f)
+        return self
+
     @property
     def state(self):
         return SimulationState(self.geometry, self.tile_grid, self.store, self.iteration,
@@ -380,7 +419,8 @@ def step(state):
     return state
 
 
-def run(config, geometry, iterations, outputs=None, device=None, check_every=STATUS_RING):
+def run(config, geometry, iterations, outputs=None, device=None, check_every=STATUS_RING,
+        resume_from=None, graph=False):
     """Iterate ``iterations`` steps (SPEC.md:403-410); returns (state,
     diagnostics).
 
@@ -388,10 +428,14 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
       "convergence_every": k   relative L2 change of u every k steps
       "tolerance": eps         stop early once that change is below eps
       "vtk": path, "csv": path write the final rho/u (legacy VTK / CSV slice)
+      "checkpoint": path       save the final state (Solver.save_checkpoint)
     Zero iterations return the initial state unchanged.
+    ``resume_from``: a checkpoint path; ``iterations`` more steps are run from
+    it.  ``graph``: replay CUDA graphs of GRAPH_STEPS steps (Solver.step).
     """
     from .output import ConvergenceEstimator, dense_macroscopic, write_csv_slice, write_vtk
-    solver = Solver(geometry, config, device)
+    solver = (Solver(geometry, config, device) if resume_from is None
+              else resume(resume_from, geometry, config, device))
     opts = outputs if isinstance(outputs, dict) else {}
     every = int(opts.get("convergence_every") or 0)
     tol = opts.get("tolerance")
@@ -402,7 +446,7 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
     converged = False
     while left > 0:
         k = min(left, every if every > 0 else check_every)
-        solver.run(k, check_every=check_every)
+        solver.run(k, check_every=check_every, graph=graph)
         left -= k
         if est is not None:
             change = est()
@@ -413,6 +457,8 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
                    "guard_iterations": list(solver.guard_iterations),
                    "convergence": list(est.history) if est is not None else [],
                    "converged": converged}
+    if opts.get("checkpoint"):
+        solver.save_checkpoint(opts["checkpoint"])
     if opts.get("vtk") or opts.get("csv"):
         rho, u = dense_macroscopic(solver)
         if opts.get("vtk"):
@@ -422,6 +468,33 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
     if callable(outputs):
         outputs(solver)
     return solver.state, diagnostics
+
+
+CHECKPOINT_FORMAT = "tlbm-checkpoint-1"
+
+
+def geometry_fingerprint(geometry):
+    """sha256 over the voxel tags, shape, boundary values and periodic flags."""
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(geometry.types, dtype=np.uint8).tobytes())
+    h.update(json.dumps([list(geometry.shape), [float(v) for v in geometry.inlet_velocity],
+                         float(geometry.outlet_density),
+                         [bool(p) for p in geometry.periodic]]).encode())
+    return h.hexdigest()
+
+
+def resume(path, geometry, config=None, device=None):
+    """A Solver restored from a checkpoint; ``config`` defaults to the one
+    stored in the checkpoint."""
+    if config is None:
+        with np.load(path, allow_pickle=False) as z:
+            kw = json.loads(str(z["config"]))
+            if "mrt_matrix" in z.files:
+                kw["mrt_matrix"] = z["mrt_matrix"]
+        if kw.get("mrt_relaxation") is not None:
+            kw["mrt_relaxation"] = tuple(kw["mrt_relaxation"])
+        config = SimulationConfig(**kw)
+    return Solver(geometry, config, device).load_checkpoint(path)
 
 
 def rest_weights(dtype=np.float64):

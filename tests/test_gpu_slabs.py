@@ -97,7 +97,39 @@ def test_slab_channel_single_rank_runs():
     assert run.n_fn_owned == 32 ** 3 and s.iteration == 5
 
 
-def _mp_worker(rank, world, port, steps, out, transport="gloo"):
+COLLISIONS = {"lbgk": {}, "mrt": {"collision": "mrt"},
+              "mrt_fma": {"collision": "mrt", "arithmetic": "fma"},
+              "lbgk_fma_quasi": {"arithmetic": "fma", "fluid": "quasi-compressible"}}
+
+
+@pytest.mark.parametrize("coll", [c for c in COLLISIONS if c != "lbgk"])
+@pytest.mark.parametrize("name", ["pack_io", "chan_periodic"])
+def test_virtual_slabs_collision_modes(name, coll):
+    """MRT and FMA arithmetic through the slab decomposition: bit-identical
+    to the single-domain step with the same configuration."""
+    geo = CASES[name]()
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
+    f0 = _f0(geo, np.float64)
+    ref = solver.Solver(geo, cfg)
+    ref.set_fields_canonical(dense.to_canonical(f0, ref.tile_grid.non_empty, np.zeros(19)))
+    ref.step(8)
+    want = ref.to_dense(ref.fields_canonical(device=True))
+    vs = slabs.VirtualSlabs(geo, 3, cfg)
+    for sl in vs.slabs:
+        s = sl.solver
+        fl = _local_f(f0, sl.range, geo.shape[2])
+        s.set_fields_canonical(dense.to_canonical(fl, s.tile_grid.non_empty, np.zeros(19)))
+    vs.step(8)
+    got = torch.zeros_like(want)
+    for sl in vs.slabs:
+        d = sl.solver.to_dense(sl.solver.fields_canonical(device=True))
+        lo = TILE if sl.range.lower >= 0 else 0
+        got[..., sl.range.z0:sl.range.z1] = d[..., lo:lo + sl.range.z1 - sl.range.z0]
+    mask = torch.from_numpy(geo.types != 0).cuda()
+    assert torch.equal(got[:, mask], want[:, mask])
+
+
+def _mp_worker(rank, world, port, steps, out, transport="gloo", coll="lbgk"):
     import os
 
     import torch.distributed as dist
@@ -105,7 +137,7 @@ def _mp_worker(rank, world, port, steps, out, transport="gloo"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     geo = CASES["pack_io"]()
-    cfg = solver.SimulationConfig(u_max_guard=0.0)
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
     run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport=transport)
     s = run.slab.solver
     f0 = _f0(geo, np.float64)
@@ -126,9 +158,10 @@ def _mp_worker(rank, world, port, steps, out, transport="gloo"):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("transport", ["gloo", "ipc"])
+@pytest.mark.parametrize("transport,coll", [("gloo", "lbgk"), ("ipc", "lbgk"), ("ipc", "mrt"),
+                                            ("ipc", "mrt_fma")])
 @pytest.mark.parametrize("world", [2, 3])
-def test_multiprocess_runner_on_one_gpu(world, transport):
+def test_multiprocess_runner_on_one_gpu(world, transport, coll):
     """DistributedSlabRunner in `world` processes sharing cuda:0 == the
     single-domain step.  transport "gloo": halo staged through host memory;
     "ipc": the fused peer-store halo over CUDA IPC mappings with the
@@ -143,7 +176,7 @@ def test_multiprocess_runner_on_one_gpu(world, transport):
     steps = 10
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
-    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, steps, out, transport))
+    procs = [ctx.Process(target=_mp_worker, args=(r, world, port, steps, out, transport, coll))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -151,7 +184,7 @@ def test_multiprocess_runner_on_one_gpu(world, transport):
         p.join(300)
         assert p.exitcode == 0
     geo = CASES["pack_io"]()
-    cfg = solver.SimulationConfig(u_max_guard=0.0)
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
     ref = solver.Solver(geo, cfg)
     ref.set_fields_canonical(dense.to_canonical(_f0(geo, np.float64), ref.tile_grid.non_empty,
                                                 np.zeros(19)))

@@ -108,3 +108,15 @@ def test_step_args_layout_matches_header(tmp_path):
                                           check=True).stdout.split()]
     want = [getattr(nat.StepArgs, n).offset for n in names] + [ctypes.sizeof(nat.StepArgs)]
     assert got == want
+
+
+def test_geometry_fingerprint_distinguishes_inputs():
+    from paper_1611_02445_b200 import geometry, solver
+    a = geometry.generate_cavity3d(8)
+    assert solver.geometry_fingerprint(a) == solver.geometry_fingerprint(
+        geometry.generate_cavity3d(8))
+    assert solver.geometry_fingerprint(a) != solver.geometry_fingerprint(
+        geometry.generate_cavity3d(8, lid_velocity=(0.04, 0.0, 0.0)))
+    t = a.types.copy()
+    t[3, 3, 3] = 0
+    assert solver.geometry_fingerprint(a) != solver.geometry_fingerprint(geometry.Geometry(t))
