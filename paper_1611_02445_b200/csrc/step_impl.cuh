@@ -108,8 +108,33 @@ constexpr int min_blocks() {
     return warps / (2 * tiles_per_cta<T>());
 }
 
+// TLBM_LOAD_MODE (tuning knob): 0 ld.global.nc (default), 1 ld.global,
+// 2 ld.global.nc with an L2 evict_last hint
+#ifndef TLBM_LOAD_MODE
+#define TLBM_LOAD_MODE 0
+#endif
 template <class T>
-__device__ __forceinline__ T load_ro(const T *p) { return __ldg(p); }
+__device__ __forceinline__ T load_ro(const T *p) {
+#if TLBM_LOAD_MODE == 1
+    T v;
+    if constexpr (sizeof(T) == 8)
+        asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    else
+        asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#elif TLBM_LOAD_MODE == 2
+    T v;
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (sizeof(T) == 8)
+        asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 
 // Hide how a pointer was formed so the compiler keeps it as one 64-bit
 // register (base + 32-bit offset -> a single IMAD.WIDE per access) instead of

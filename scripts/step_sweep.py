@@ -26,11 +26,16 @@ p.add_argument("--porosity", type=float, default=0.5)
 p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
 p.add_argument("--arith", default="reference", choices=["reference", "fma"])
 p.add_argument("--graph", action="store_true", help="replay captured CUDA graphs of steps")
+p.add_argument("--l2-fetch", type=int, default=-1,
+               help="cudaLimitMaxL2FetchGranularity in bytes (0..128; -1 leaves the default)")
 a = p.parse_args()
 if a.geometry == "channel":
     geo = workloads.channel(a.n)
 elif a.geometry == "channel_z":
     geo = workloads.channel_z(a.n, a.length)
+elif a.geometry == "duct_z":        # walled square duct along z (no periodic wrap)
+    from paper_1611_02445_b200 import geometry as _g
+    geo = _g.generate_channel("square", a.n, axis=2, length=a.length or a.n, ends="wall")
 elif a.geometry == "cavity":
     geo = workloads.cavity(a.n)
 else:
@@ -40,6 +45,12 @@ s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0
 if a.no_perturb:
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04) if a.geometry == "channel_z" else (0.04, 0.0, 0.0))
 from paper_1611_02445_b200.solver import GRAPH_STEPS as solver_graph_steps  # noqa: E402
+l2_fetch = None
+if a.l2_fetch >= 0:
+    nat.call("tlbm_set_l2_fetch_granularity", a.l2_fetch)
+    _v = nat.ctypes.c_int()
+    nat.call("tlbm_get_l2_fetch_granularity", nat.ctypes.byref(_v))
+    l2_fetch = _v.value
 vmap = {"full": nat.FULL, "prop": nat.PROPAGATION_ONLY, "rw": nat.READ_WRITE_ONLY,
         "mrt": nat.FULL}
 n_d = 8 if a.precision == "f64" else 4
@@ -63,7 +74,7 @@ for v in a.variants.split(","):
     mlups = s.n_fn / (ms / 1e3) / 1e6
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
     print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
-                      "arith": a.arith, "graph": a.graph,
+                      "arith": a.arith, "graph": a.graph, "l2_fetch": l2_fetch,
                       "geometry": a.geometry, "n": a.n, "dims": list(geo.shape),
                       "field_gb": round(2 * s.t_n * 19 * 64 * n_d / 1e9, 2),
                       "precision": a.precision, "table": a.table, "variant": v,
