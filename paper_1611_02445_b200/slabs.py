@@ -255,11 +255,13 @@ class IpcHalo:
     The boundary-layer step kernel stores its outgoing z planes directly
     into the neighbours' ghost tiles (tlbm_step_args.halo_*): no pack kernel,
     no staging buffer, no copy engine, no NCCL on the step path.  Ordering is
-    a stream-ordered step counter per neighbour pair: before step t a rank
+    a stream-ordered step counter per neighbour pair.  Step t runs the
+    interior tiles first (own tiles only, no neighbour needed); then the rank
     waits (tlbm_peer_wait) until both neighbours published t, i.e. finished
-    step t-1 -- so their ghost planes of the copy it reads are written, and
-    they no longer read the copy whose ghosts it is about to write -- and after
-    step t it publishes t+1 into their inboxes (tlbm_peer_signal, system-scope
+    the boundary layers of step t-1 -- so their ghost planes of the copy it
+    reads are written, and they no longer read the copy whose ghosts it is
+    about to write -- runs its boundary layers with the fused peer stores,
+    and publishes t+1 into their inboxes (tlbm_peer_signal, system-scope
     fence first).  A wait that exceeds ``timeout_s`` sets an error word and
     returns (checked by ``check``) instead of hanging the GPU.
     """
@@ -454,12 +456,16 @@ class DistributedSlabRunner:
                 sl.finish()
                 continue
             if self.ipc is not None:
+                # interior first: it reads and writes only this rank's own
+                # tiles, so it needs no neighbour and covers any skew
+                # between ranks; then the wait, the boundary layers with the
+                # fused peer stores, and the signal right after them
                 it = sl.solver.iteration
+                sl.step_interior()
                 self.ipc.wait(it)
                 self.ipc.arm()
                 sl.step_boundary()
                 self.ipc.disarm()
-                sl.step_interior()
                 self.ipc.signal(it + 1)
                 sl.finish()
                 continue
