@@ -185,9 +185,27 @@ typedef struct {
     const int64_t *iter_counter;
     int64_t iter_add;
     int ring_len;
+    /* compact tile storage (crank NULL = the paper's 64-slot blocks): the
+     * copies hold only non-solid slots in XYZ order, tile t's 19 blocks at
+     * cbase[t] (element offset), each cnf[t] values long, slot j at rank
+     * crank[t][j] (tlbm_compact_ranks).  Table xyz only; no fused halo. */
+    const int64_t *cbase;
+    const int32_t *cnf;
+    const uint8_t *crank;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);
+/* ---- compact tile storage (csrc/compact.cu; an extension of layout.py) --- */
+/* (t_n, 64) uint8: rank[t][j] = non-solid slots of tile t before slot j
+ * (255 for a solid slot). */
+int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank, void *stream);
+/* Convert one copy between the paper's XYZ block store ((t_n, 19, 64)
+ * blocks) and the compact store (19 * n_fn values); to_compact 1: blocks ->
+ * compact, 0: compact -> blocks (solid slots written as the rest state w_q). */
+int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, int table,
+                         int64_t t_n, const int64_t *d_base, const int32_t *d_nf,
+                         const uint8_t *d_rank, int to_compact, void *stream);
+
 /* *d_counter += k (one thread; the last node of a captured step graph). */
 int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream);
 

@@ -35,7 +35,8 @@ class StepArgs(ctypes.Structure):
                 ("halo_up", c_vp), ("halo_up_begin", c_i64), ("halo_up_end", c_i64),
                 ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
                 ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int),
-                ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int)]
+                ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int),
+                ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp)]
 
 
 _PROTOS = {
@@ -72,6 +73,9 @@ _PROTOS = {
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
     "tlbm_advance_counter": (c_int, [c_vp, c_i64, c_vp]),
+    "tlbm_compact_ranks": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "tlbm_compact_convert": (c_int, [c_vp, c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_int,
+                                     c_vp]),
     "tlbm_ipc_export": (c_int, [c_vp, c_vp, ctypes.POINTER(ctypes.c_uint64)]),
     "tlbm_ipc_import": (c_int, [c_vp, ctypes.c_uint64, ctypes.POINTER(c_vp)]),
     "tlbm_ipc_close": (c_int, [c_vp]),

@@ -58,7 +58,7 @@ def _config(args):
     from .solver import SimulationConfig
     return SimulationConfig(collision=args.model, fluid=args.fluid, tau=args.tau,
                             precision=args.precision, table=args.layout,
-                            arithmetic=args.arith)
+                            arithmetic=args.arith, storage=args.storage)
 
 
 def cmd_run(args):
@@ -170,8 +170,10 @@ def build_parser():
                         choices=["incompressible", "quasi-compressible"])
         sp.add_argument("--tau", type=float, default=0.6)
         sp.add_argument("--precision", default="f64", choices=["f64", "f32"])
-        sp.add_argument("--layout", default="b200", choices=["b200", "optimized", "xyz"])
+        sp.add_argument("--layout", default=None, choices=["b200", "optimized", "xyz"],
+                        help="default: b200 (blocks storage), xyz (compact)")
         sp.add_argument("--arith", default="reference", choices=["reference", "fma"])
+        sp.add_argument("--storage", default="blocks", choices=["blocks", "compact"])
 
     r = sub.add_parser("run")
     sim_args(r)

@@ -1,0 +1,125 @@
+// Compact tile storage (an extension of the paper's layout):
+// the field store keeps only the non-solid slots of every (tile, direction)
+// block, in the canonical (XYZ) slot order.  Tile T's 19 blocks start at
+// base(T) = 19 * (non-solid nodes of the tiles before T); block q is nf(T)
+// values long; the node at canonical slot j sits at its rank among T's
+// non-solid slots, the same in all 19 blocks:
+//     addr(T, q, j) = base(T) + q * nf(T) + rank(T, j)
+// A block of the paper's XYZ layout is the same values with the solid slots
+// left in place.
+//
+// This file: the per-tile rank bytes and the conversion between the paper's
+// block store ([tile][q][64], layout.py:115-132) and the compact one, which
+// is how every canonical read/write (init, readout, checkpoints) reaches a
+// compact store.  The compact step kernel is in step_compact.cuh.
+#include "common.cuh"
+#include "d3q19.cuh"
+
+namespace tlbm {
+namespace {
+
+constexpr int TILE_VALUES = Q * 64;
+
+// rank[t][j] = number of non-solid slots of tile t before slot j (255 for a
+// solid slot); one warp per tile, a ballot gives the tile's 64-bit mask
+__global__ void ranks_kernel(const uint32_t *meta, long long t_n, unsigned char *rank) {
+    const long long t = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= t_n) return;
+    const bool a0 = meta[t * 64 + lane] & META_ACTIVE;
+    const bool a1 = meta[t * 64 + 32 + lane] & META_ACTIVE;
+    const unsigned lo = __ballot_sync(0xffffffffu, a0), hi = __ballot_sync(0xffffffffu, a1);
+    const unsigned below = (1u << lane) - 1u;
+    rank[t * 64 + lane] = a0 ? (unsigned char)__popc(lo & below) : 255;
+    rank[t * 64 + 32 + lane] = a1 ? (unsigned char)(__popc(lo) + __popc(hi & below)) : 255;
+}
+
+template <class T, bool TO_COMPACT>
+__global__ void convert_kernel(const T *in, T *out, long long t_n, const long long *base,
+                               const int *nf, const unsigned char *rank) {
+    const long long n = t_n * 64;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+        const int r = rank[i];
+        if (r == 255) {
+            if (!TO_COMPACT) {
+                // solid slots do not exist in a compact store; expand them as
+                // the rest state w_q (rho 1, u 0), what a never-written slot
+                // of the paper's store holds after the cold start
+#pragma unroll
+                for (int q = 0; q < Q; ++q) out[t * TILE_VALUES + q * 64 + j] = T(weight(q));
+            }
+            continue;
+        }
+        const long long b = base[t] + r;
+        const int n_t = nf[t];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const long long c = b + (long long)q * n_t;
+            const long long f = t * TILE_VALUES + q * 64 + j;
+            if (TO_COMPACT) out[c] = in[f];
+            else out[f] = in[c];
+        }
+    }
+}
+
+unsigned grid_for_slots(long long n) {
+    long long g = (n + 255) / 256;
+    if (g < 1) g = 1;
+    if (g > 148LL * 32) g = 148LL * 32;
+    return (unsigned)g;
+}
+
+template <class T>
+int convert_as(const void *in, void *out, int64_t t_n, const int64_t *base, const int32_t *nf,
+               const uint8_t *rank, int to_compact, cudaStream_t s) {
+    const auto *b = reinterpret_cast<const long long *>(base);
+    if (to_compact)
+        convert_kernel<T, true><<<grid_for_slots(t_n * 64), 256, 0, s>>>(
+            static_cast<const T *>(in), static_cast<T *>(out), t_n, b, nf, rank);
+    else
+        convert_kernel<T, false><<<grid_for_slots(t_n * 64), 256, 0, s>>>(
+            static_cast<const T *>(in), static_cast<T *>(out), t_n, b, nf, rank);
+    return launch_check("convert_kernel");
+}
+
+}  // namespace
+}  // namespace tlbm
+
+using namespace tlbm;
+
+extern "C" int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank,
+                                  void *stream) {
+    if (!d_meta || !d_rank || t_n < 0) {
+        set_error("tlbm_compact_ranks: bad argument");
+        return TLBM_ERR_ARG;
+    }
+    if (t_n == 0) return TLBM_OK;
+    ranks_kernel<<<(unsigned)((t_n * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
+        d_meta, (long long)t_n, d_rank);
+    return launch_check("ranks_kernel");
+}
+
+extern "C" int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, int table,
+                                    int64_t t_n, const int64_t *d_base, const int32_t *d_nf,
+                                    const uint8_t *d_rank, int to_compact, void *stream) {
+    int rc;
+    if ((rc = check_dtype(dtype)) || (rc = check_table(table))) return rc;
+    if (!compact_table_ok(table)) {
+        set_error("compact storage keeps blocks in XYZ order: needs the xyz table, got %d",
+                  table);
+        return TLBM_ERR_ARG;
+    }
+    if (!d_in || !d_out || !d_base || !d_nf || !d_rank) {
+        set_error("tlbm_compact_convert: null argument");
+        return TLBM_ERR_ARG;
+    }
+    if (t_n == 0) return TLBM_OK;
+    cudaStream_t s = as_stream(stream);
+    return dtype == TLBM_F64 ? convert_as<double>(d_in, d_out, t_n, d_base, d_nf, d_rank,
+                                                  to_compact, s)
+                             : convert_as<float>(d_in, d_out, t_n, d_base, d_nf, d_rank,
+                                                 to_compact, s);
+}

@@ -62,6 +62,10 @@ __host__ __device__ constexpr int kind_of(int table, int q) {
          : K_YXZ;
 }
 
+// compact storage (compact.cu, step_compact.cuh) keeps every block in the
+// canonical XYZ slot order, so a node's rank is one number for all 19 blocks
+__host__ __device__ constexpr bool compact_table_ok(int table) { return table == T_XYZ; }
+
 template <int TABLE>
 __device__ __forceinline__ int slot_of(int q, int x, int y, int z) {
     return layout_slot(kind_of(TABLE, q), x, y, z);

@@ -1,0 +1,161 @@
+// The fused step on the compact tile store (compact.cu): the same pull
+// gather, boundary handling, collision and store as step_kernel
+// (step_impl.cuh), with every block holding only its tile's non-solid slots.
+//
+// Why: on a sparse geometry the paper's 64-slot blocks put solid slots next
+// to fluid ones, so DRAM moves whole 32-byte sectors of which part is never
+// used, and partially written sectors cost a fill read.  Packing the blocks
+// removes both: scripts/sparse_traffic_model.py gives 152 B read + 152 B
+// written per fluid node at every porosity (fp64), against 177 + 177 B plus
+// 1.5 partial sectors per node at porosity 0.2 in the paper's layout.
+//
+// In-block order: the compact store keeps every block in the canonical
+// (XYZ) slot order, so a node's rank -- its index among its tile's non-solid
+// slots -- is the same in all 19 blocks of the tile.  The per-layout sector
+// tricks of the B200 table do not apply once blocks are packed; packing is
+// what removes the over-fetch.
+//
+// Addressing per pull (direction q, packed word w of the XYZ pull table):
+//   link:    source tile k = neighbour row entry w >> 22, slot s = w & 63,
+//            block q
+//   no link: own tile, the node's own slot, block opp(q)
+//   addr = base(k) + block * nf(k) + rank(k, s)
+// The CTA stages base/nf and the 64 one-byte ranks (crank, built at setup)
+// of the 27 neighbour tiles in shared memory, so a pull's rank is one byte
+// load from shared memory.
+#pragma once
+
+namespace tlbm {
+namespace step_detail {
+
+// occupancy of the compact kernel (resident warps per SM): the rank
+// arithmetic needs more registers than the block-store kernel, so fp32 runs
+// at 32 warps/SM (64 registers; at 64 warps it spilled 240 bytes)
+#ifndef TLBM_WARPS_COMPACT
+#define TLBM_WARPS_COMPACT 32
+#endif
+#ifndef TLBM_WARPS_COMPACT_F32
+#define TLBM_WARPS_COMPACT_F32 32
+#endif
+// per (q, j): 64 * (neighbour-row entry of the source tile) + source slot
+struct CompactPull {
+    uint16_t w[Q * 64];
+};
+constexpr CompactPull make_compact_pull() {
+    CompactPull t{};
+    for (int q = 0; q < Q; ++q)
+        for (int j = 0; j < 64; ++j) {
+            const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
+            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
+            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
+            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
+            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
+            t.w[q * 64 + j] = (uint16_t)(64 * delta_index(dx, dy, dz) +
+                                         ((sx & 3) + 4 * (sy & 3) + 16 * (sz & 3)));
+        }
+    return t;
+}
+__device__ const CompactPull kCompactPull = make_compact_pull();
+
+#ifndef TLBM_TPC_COMPACT
+#define TLBM_TPC_COMPACT 2
+#endif
+template <class T>
+constexpr int compact_tiles_per_cta() { return sizeof(T) == 4 ? 1 : TLBM_TPC_COMPACT; }
+
+template <class T, bool MRT, int VARIANT>
+constexpr int min_blocks_compact() {
+    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32 : TLBM_WARPS_MRT)
+                : (sizeof(T) == 4 ? TLBM_WARPS_COMPACT_F32 : TLBM_WARPS_COMPACT)) /
+           (2 * compact_tiles_per_cta<T>());
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA>
+__global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT>())
+step_kernel_compact(const StepParams<T, MRT> p) {
+    static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
+    __shared__ const T *s_src[TPC][NBR];
+    __shared__ int s_nf[TPC][NBR];
+    __shared__ __align__(16) unsigned char s_rank[TPC][NBR][64];
+    const int ti = threadIdx.x >> 6;
+    const int j = threadIdx.x & 63;
+    const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
+    const long long tile = tile0 + ti;
+
+    // the node word does not depend on the staging: load it first so its
+    // latency overlaps the neighbour rows
+    const uint32_t meta = tile < p.tile_end ? p.meta[tile * 64 + j] : 0u;
+    // neighbour rows, then each neighbour's 64 ranks as four 16-byte copies
+    for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
+        const long long t = tile0 + i / NBR;
+        const int k = i % NBR;
+        long long nb = -1;
+        if (t < p.tile_end) nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1)
+                                                                  : p.nbr[t * NBR + k];
+        const long long tt = nb >= 0 ? nb : (t < p.tile_end ? t : p.tile_begin);
+        s_src[i / NBR][k] = p.src + p.cbase[tt];
+        s_nf[i / NBR][k] = p.cnf[tt];
+        const uint4 *r = reinterpret_cast<const uint4 *>(p.crank + tt * 64);
+        uint4 *d = reinterpret_cast<uint4 *>(&s_rank[i / NBR][k][0]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) d[c] = __ldg(r + c);
+    }
+    __syncthreads();
+
+    uint32_t status = 0;
+    if (meta & META_ACTIVE) {
+        const T *own_src = s_src[ti][13];
+        const int nf_own = s_nf[ti][13];
+        const int rank_own = s_rank[ti][13][j];
+        T g[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
+                g[q] = load_ro(own_src + (q * nf_own + rank_own));
+                continue;
+            }
+            // w = 64 * (source tile entry) + source slot
+            const uint32_t w = __ldg(&kCompactPull.w[q * 64 + j]);
+            const bool link = (meta >> q) & 1u;
+            const int k = link ? (int)(w >> 6) : 13;
+            const int rank = link ? (int)(&s_rank[ti][0][0])[w] : rank_own;
+            const int blk = link ? q : opp(q);
+            g[q] = load_ro(s_src[ti][k] + (blk * s_nf[ti][k] + rank));
+        }
+
+        if (VARIANT == TLBM_FULL) {
+            const int tag = meta_type(meta);
+            if (tag == BB_WALL) {
+#pragma unroll
+                for (int q = 1; q < Q; ++q)
+                    if (q < opp(q)) { T t = g[q]; g[q] = g[opp(q)]; g[opp(q)] = t; }
+            } else {
+                if (tag == INLET || tag == OUTLET)
+                    zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
+                if constexpr (MRT && FMA)
+                    status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                else if constexpr (MRT)
+                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                else if constexpr (FMA)
+                    status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
+                else
+                    status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
+            }
+        }
+        T *out = p.dst + (own_src - p.src);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
+    }
+    if (p.flags) {
+        const uint32_t any = __reduce_or_sync(0xffffffffu, status);
+        if (any && (threadIdx.x & 31) == 0) {
+            uint32_t *f = p.flags;
+            if (p.iter)
+                f += (unsigned long long)(*p.iter + p.iter_add) % p.ring_len;
+            if (any & ~*reinterpret_cast<volatile uint32_t *>(f)) atomicOr(f, any);
+        }
+    }
+}
+
+}  // namespace step_detail
+}  // namespace tlbm

@@ -52,6 +52,10 @@ struct StepParams {
     long long halo_up_begin, halo_up_end;
     T *halo_down;           // e_z = -1 directions of plane z = 0
     long long halo_down_begin, halo_down_end;
+    // compact tile storage (compact.cu, step_compact.cuh); null otherwise
+    const long long *__restrict__ cbase;
+    const int *__restrict__ cnf;
+    const unsigned char *__restrict__ crank;
 };
 
 __host__ __device__ constexpr int up_dir(int k) {
@@ -323,8 +327,17 @@ step_kernel(const StepParams<T, MRT> p) {
     }
 }
 
+}  // namespace step_detail
+}  // namespace tlbm
+#include "step_compact.cuh"
+namespace tlbm {
+namespace step_detail {
+
 template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO, bool FMA>
 int launch_as(const tlbm_step_args *a, cudaStream_t s);
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool MRT>
+int launch_compact(const tlbm_step_args *a, cudaStream_t s);
 
 template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool FMA>
 int launch_halo(const tlbm_step_args *a, cudaStream_t s) {
@@ -344,6 +357,15 @@ int launch_arith(const tlbm_step_args *a, cudaStream_t s) {
 
 template <class T, int QUASI, int TABLE, int VARIANT>
 int launch(const tlbm_step_args *a, cudaStream_t s) {
+    if (a->crank) {
+        if constexpr (compact_table_ok(TABLE)) {
+            if (VARIANT == TLBM_FULL && a->collision == TLBM_MRT)
+                return launch_compact<T, QUASI, TABLE, VARIANT, VARIANT == TLBM_FULL>(a, s);
+            return launch_compact<T, QUASI, TABLE, VARIANT, false>(a, s);
+        }
+        set_error("tlbm_step: compact storage needs the xyz layout table");
+        return TLBM_ERR_ARG;
+    }
     if (VARIANT == TLBM_FULL && a->collision == TLBM_MRT) {
         if (a->rel32) return launch_arith<T, QUASI, TABLE, VARIANT, true, true>(a, s);
         return launch_arith<T, QUASI, TABLE, VARIANT, false, true>(a, s);
@@ -353,9 +375,51 @@ int launch(const tlbm_step_args *a, cudaStream_t s) {
     return launch_arith<T, QUASI, TABLE, VARIANT, false, false>(a, s);
 }
 
+template <class T, bool MRT, bool FMA>
+void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a);
+
 template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO, bool FMA>
 int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
+    fill_params<T, MRT, FMA>(p, a);
+    const long long n = a->tile_end - a->tile_begin;
+    if (n <= 0) return TLBM_OK;
+    constexpr int TPC = tiles_per_cta<T>();
+    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA>
+        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+    return launch_check("step_kernel");
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA>
+int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
+    StepParams<T, MRT> p;
+    fill_params<T, MRT, FMA>(p, a);
+    const long long n = a->tile_end - a->tile_begin;
+    if (n <= 0) return TLBM_OK;
+    constexpr int TPC = compact_tiles_per_cta<T>();
+    step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA>
+        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+    return launch_check("step_kernel_compact");
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool MRT>
+int launch_compact(const tlbm_step_args *a, cudaStream_t s) {
+    if (a->halo_up || a->halo_down) {
+        set_error("tlbm_step: the fused halo does not support compact storage");
+        return TLBM_ERR_ARG;
+    }
+    if (!a->cbase || !a->cnf) {
+        set_error("tlbm_step: compact storage needs cbase, cnf and crank");
+        return TLBM_ERR_ARG;
+    }
+    constexpr bool kFma = VARIANT == TLBM_FULL && sizeof(T) == 8;
+    if (kFma && a->arith == TLBM_ARITH_FMA)
+        return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, kFma>(a, s);
+    return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, false>(a, s);
+}
+
+template <class T, bool MRT, bool FMA>
+void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     if constexpr (MRT)
         for (int k = 0; k < Q * Q; ++k) p.mrt.op[k] = T(a->mrt_op[k]);   // op.astype(dtype)
     p.src = static_cast<const T *>(a->f_src);
@@ -378,12 +442,9 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     p.halo_down = static_cast<T *>(a->halo_down);
     p.halo_down_begin = a->halo_down_begin;
     p.halo_down_end = a->halo_down_end;
-    const long long n = a->tile_end - a->tile_begin;
-    if (n <= 0) return TLBM_OK;
-    constexpr int TPC = tiles_per_cta<T>();
-    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA>
-        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
-    return launch_check("step_kernel");
+    p.cbase = reinterpret_cast<const long long *>(a->cbase);
+    p.cnf = a->cnf;
+    p.crank = a->crank;
 }
 
 template <class T>

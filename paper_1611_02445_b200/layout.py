@@ -188,3 +188,82 @@ class FieldStore:
         nat.call("tlbm_to_canonical", nat.ptr(self.copy_tensor(copy)), self.code,
                  TABLE_CODE[self.table], self.t_n, nat.ptr(out), nat.stream_ptr(self.device))
         return out if device else out.cpu().numpy()
+
+
+class CompactFieldStore(FieldStore):
+    """Two copies holding only the non-solid slots of every block, in the
+    canonical XYZ slot order (an extension of the paper's layout;
+    csrc/compact.cu).  Tile t's 19 blocks start at ``base[t]`` = 19 x
+    (non-solid nodes of the tiles before t), each ``nf[t]`` values long, slot
+    j at ``rank[t, j]`` (its index among the tile's non-solid slots, 255 for
+    a solid slot).  ``flat`` holds 2 x 19 x n_fn values.
+
+    Canonical I/O goes through the paper's block layout: ``to_blocks`` /
+    ``from_blocks`` convert one copy to and from a (t_n, 19, 64) XYZ block
+    store, whose solid slots read as the rest state w_q."""
+
+    def __init__(self, tiling, table=LayoutTable.XYZ, dtype=np.float64):
+        if table is not LayoutTable.XYZ:
+            raise ValueError(f"compact storage keeps blocks in XYZ order; table must be xyz, "
+                             f"not {table.value}")
+        self.device = nat.require_cuda(tiling.device)
+        self.t_n = int(tiling.t_n)
+        self.n_fn = int(tiling.n_fn)
+        self.table = table
+        self.dtype = np.dtype(dtype)
+        self.code = nat.code_of(self.dtype)
+        self.tdtype = nat.torch_dtype(self.code)
+        self.perms = table_permutations(table)
+        self.nf = tiling.counts
+        base = torch.zeros(max(self.t_n, 1), dtype=torch.int64, device=self.device)
+        if self.t_n > 1:
+            base[1:self.t_n] = torch.cumsum(self.nf[:-1].to(torch.int64), 0) * Q
+        self.base = base[:self.t_n]
+        self.rank = torch.empty((max(self.t_n, 1), 64), dtype=torch.uint8,
+                                device=self.device)[:self.t_n]
+        nat.call("tlbm_compact_ranks", nat.ptr(tiling.meta), self.t_n, nat.ptr(self.rank),
+                 nat.stream_ptr(self.device))
+        self.flat = torch.empty(2 * Q * self.n_fn, dtype=self.tdtype, device=self.device)
+
+    def copy_tensor(self, copy):
+        if int(copy) not in (0, 1):
+            raise ValueError(f"copy flag must be 0 or 1: {copy}")
+        n = Q * self.n_fn
+        return self.flat[int(copy) * n:(int(copy) + 1) * n]
+
+    def _convert(self, src, dst, to_compact):
+        nat.call("tlbm_compact_convert", nat.ptr(src), nat.ptr(dst), self.code,
+                 TABLE_CODE[self.table], self.t_n, nat.ptr(self.base), nat.ptr(self.nf),
+                 nat.ptr(self.rank), int(to_compact), nat.stream_ptr(self.device))
+
+    def to_blocks(self, copy):
+        """One copy expanded to the paper's (t_n*19*64,) block store (a new
+        tensor; solid slots hold the rest state w_q)."""
+        out = torch.empty(self.t_n * Q * 64, dtype=self.tdtype, device=self.device)
+        self._convert(self.copy_tensor(copy), out, False)
+        return out
+
+    def from_blocks(self, copy, blocks):
+        self._convert(blocks, self.copy_tensor(copy), True)
+
+    def blocks(self, copy):
+        """(t_n, 19, 64) blocks of one copy (an expanded copy, not a view)."""
+        return self.to_blocks(copy).view(self.t_n, Q, 64)
+
+    def fill_canonical(self, copy, values):
+        nat.require_cuda(self.device)
+        src = _as_device(values, self.tdtype, self.device)
+        if tuple(src.shape) != (Q, self.t_n, 64):
+            raise ValueError(f"expected shape (19, {self.t_n}, 64), got {tuple(src.shape)}")
+        tmp = torch.empty(self.t_n * Q * 64, dtype=self.tdtype, device=self.device)
+        nat.call("tlbm_from_canonical", nat.ptr(src), self.code, TABLE_CODE[self.table],
+                 self.t_n, nat.ptr(tmp), nat.stream_ptr(self.device))
+        self.from_blocks(copy, tmp)
+
+    def read_canonical(self, copy, device=False):
+        nat.require_cuda(self.device)
+        tmp = self.to_blocks(copy)
+        out = torch.empty((Q, self.t_n, 64), dtype=self.tdtype, device=self.device)
+        nat.call("tlbm_to_canonical", nat.ptr(tmp), self.code, TABLE_CODE[self.table],
+                 self.t_n, nat.ptr(out), nat.stream_ptr(self.device))
+        return out if device else out.cpu().numpy()

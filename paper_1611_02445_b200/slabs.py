@@ -130,6 +130,10 @@ class SlabSolver:
         self.plan, self.rank = plan, rank
         self.range = plan.ranges[rank]
         self.local_geometry = plan.local_geometry(geometry, rank)
+        if config is not None and config.storage != "blocks":
+            raise ValueError("slab decomposition needs the block storage (storage='blocks'): "
+                             "halo pack/unpack and the fused peer stores address 64-slot "
+                             "blocks")
         self.solver = Solver(self.local_geometry, config or SimulationConfig(), device)
         s = self.solver
         layers = layer_tile_ranges(s.tiling.tile_map)

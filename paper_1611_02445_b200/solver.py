@@ -10,7 +10,10 @@ step semantics are restated in SURVEY Appendix A).  API:
                       unfused operation order, bit-identical to the
                       reference) or "fma" (fused multiply-adds in the
                       collision: fewer instructions, parity within the
-                      stated 1e-12 tolerance; f64 only).
+                      stated 1e-12 tolerance; f64 only), and ``storage``:
+                      "blocks" (default, the paper's 64-slot blocks) or
+                      "compact" (only the non-solid slots of every block;
+                      less DRAM traffic on sparse geometries, single GPU).
 ``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,
                       iteration, parity).
 ``Solver``            owns the device state; ``step(n)``, ``run(n)``,
@@ -36,7 +39,7 @@ import torch
 from . import _native as nat
 from .collision import CollisionModel, DivergenceError, FluidModel, fluid_code
 from .geometry import Geometry
-from .layout import TABLE_CODE, FieldStore, LayoutTable
+from .layout import TABLE_CODE, CompactFieldStore, FieldStore, LayoutTable
 from .lattice import Q, WEIGHTS
 from .tiling import DeviceTiling
 
@@ -56,13 +59,16 @@ class SimulationConfig:
     mrt_relaxation: tuple = None
     precision: str = "f64"
     u_max_guard: float = 0.05
-    table: LayoutTable = LayoutTable.B200
+    table: LayoutTable = None      # default: B200 (blocks storage), XYZ (compact)
     mrt_matrix: object = None      # optional explicit 19x19 operator (overrides rates)
     arithmetic: str = "reference"  # "reference" (bit-exact) | "fma"
+    storage: str = "blocks"        # "blocks" (the paper's 64-slot blocks) | "compact"
 
     def __post_init__(self):
         self.collision = CollisionModel(getattr(self.collision, "value", self.collision))
         self.fluid = FluidModel(getattr(self.fluid, "value", self.fluid))
+        if self.table is None:
+            self.table = LayoutTable.XYZ if self.storage == "compact" else LayoutTable.B200
         self.table = LayoutTable(getattr(self.table, "value", self.table))
         if not float(self.tau) > 0.5:
             raise ValueError(f"relaxation time must exceed 0.5: {self.tau}")
@@ -70,6 +76,10 @@ class SimulationConfig:
             raise ValueError(f"unknown precision: {self.precision!r}")
         if self.arithmetic not in ("reference", "fma"):
             raise ValueError(f"unknown arithmetic: {self.arithmetic!r}")
+        if self.storage not in ("blocks", "compact"):
+            raise ValueError(f"unknown storage: {self.storage!r}")
+        if self.storage == "compact" and self.table is not LayoutTable.XYZ:
+            raise ValueError("compact storage keeps blocks in XYZ order: table must be xyz")
         if self.arithmetic == "fma" and self.precision != "f64":
             raise ValueError("arithmetic='fma' is f64-only: in f32 it drifts past the 1e-5 "
                              "parity bar (u: 1.1e-5 after 1000 cavity-64 steps)")
@@ -123,8 +133,11 @@ class Solver:
         self.device = self.tiling.device
         self.t_n = self.tiling.t_n
         self.n_fn = self.tiling.n_fn
-        self.store = FieldStore(self.t_n, self.config.table, self.config.dtype, self.device,
-                                zero=False)
+        if self.config.storage == "compact":
+            self.store = CompactFieldStore(self.tiling, self.config.table, self.config.dtype)
+        else:
+            self.store = FieldStore(self.t_n, self.config.table, self.config.dtype, self.device,
+                                    zero=False)
         self.code = self.store.code
         self.fluid = fluid_code(self.config.fluid)
         self.table = TABLE_CODE[self.config.table]
@@ -146,6 +159,10 @@ class Solver:
         a.u_guard = float(self.config.u_max_guard or 0.0)
         a.rel32 = int(self.tiling.rel32 and not index64)
         a.arith = nat.ARITH_FMA if self.config.arithmetic == "fma" else nat.ARITH_REFERENCE
+        if self.config.storage == "compact":
+            a.cbase = self.store.base.data_ptr()
+            a.cnf = self.store.nf.data_ptr()
+            a.crank = self.store.rank.data_ptr()
         self._mrt_op = self.config.mrt_operator        # kept alive for the ABI pointer
         if self._mrt_op is not None:
             self._mrt_op = np.ascontiguousarray(self._mrt_op)
@@ -165,10 +182,25 @@ class Solver:
         (the conventional cold start uses rho=1, u=0)."""
         nat.require_cuda(self.device)
         for c in (0, 1):
-            nat.call("tlbm_init_equilibrium", nat.ptr(self.store.copy_tensor(c)), self.code,
+            blk = self._blocks_out(c)
+            nat.call("tlbm_init_equilibrium", nat.ptr(blk), self.code,
                      self.fluid, self.table, self.t_n, float(rho), *(float(v) for v in u),
                      nat.stream_ptr(self.device))
+            self._blocks_in(c, blk)
         self._reset_counters()
+
+    # the paper-layout blocks of one copy for the block-store kernels (init,
+    # readout): the copy itself, or an expanded temporary for compact storage
+    def _blocks_out(self, c, current=False):
+        if isinstance(self.store, CompactFieldStore):
+            if current:
+                return self.store.to_blocks(c)
+            return torch.empty(self.t_n * Q * 64, dtype=self.store.tdtype, device=self.device)
+        return self.store.copy_tensor(c)
+
+    def _blocks_in(self, c, blk):
+        if isinstance(self.store, CompactFieldStore):
+            self.store.from_blocks(c, blk)
 
     def init_from_macroscopic(self, rho, u):
         """Both copies := equilibrium(rho, u) per slot; rho (t_n, 64), u
@@ -180,9 +212,11 @@ class Solver:
         if tuple(r.shape) != (self.t_n, 64) or tuple(v.shape) != (3, self.t_n, 64):
             raise ValueError("expected rho (t_n, 64) and u (3, t_n, 64)")
         for c in (0, 1):
-            nat.call("tlbm_init_from_macroscopic", nat.ptr(self.store.copy_tensor(c)),
+            blk = self._blocks_out(c)
+            nat.call("tlbm_init_from_macroscopic", nat.ptr(blk),
                      self.code, self.fluid, self.table, self.t_n, nat.ptr(r), nat.ptr(v),
                      nat.stream_ptr(self.device))
+            self._blocks_in(c, blk)
         self._reset_counters()
 
     def set_fields_canonical(self, values, copy=None):
@@ -316,7 +350,8 @@ class Solver:
         u = torch.empty((3, self.t_n, 64), dtype=dt, device=self.device)
         p = torch.empty((self.t_n, 64), dtype=dt, device=self.device)
         flags = torch.zeros(1, dtype=torch.int32, device=self.device)
-        nat.call("tlbm_macroscopic", nat.ptr(self.store.copy_tensor(c)), self.code, self.fluid,
+        nat.call("tlbm_macroscopic", nat.ptr(self._blocks_out(c, current=True)), self.code,
+                 self.fluid,
                  self.table, self.t_n, nat.ptr(rho), nat.ptr(u), nat.ptr(p), nat.ptr(flags),
                  nat.stream_ptr(self.device))
         if self.fluid == nat.QUASI and int(flags.item()) & nat.FLAG_DIVERGED:

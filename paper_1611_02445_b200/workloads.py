@@ -59,10 +59,11 @@ def perturbed_fields(t_n, dtype, device, u0=(0.04, 0.0, 0.0), amp=1e-3, seed=123
     return rho, u
 
 
-def make_solver(geo, precision="f64", fluid="incompressible", table="b200", perturb=True,
-                device=None, u0=(0.04, 0.0, 0.0), index64=False, arithmetic="reference"):
+def make_solver(geo, precision="f64", fluid="incompressible", table=None, perturb=True,
+                device=None, u0=(0.04, 0.0, 0.0), index64=False, arithmetic="reference",
+                storage="blocks"):
     cfg = SimulationConfig(fluid=fluid, tau=TAU, precision=precision, table=table,
-                           arithmetic=arithmetic)
+                           arithmetic=arithmetic, storage=storage)
     s = Solver(geo, cfg, device=device, index64=index64)
     if perturb:
         rho, u = perturbed_fields(s.t_n, s.store.tdtype, s.device, u0)

@@ -15,6 +15,6 @@ $NV -c -o $OUT/step_f32.o $C/step_f32.cu 2> $OUT/f32.log &
 $NV -c -o $OUT/step_f64.o $C/step_f64.cu 2> $OUT/f64.log &
 wait
 O=$ROOT/paper_1611_02445_b200/lib/obj
-nvcc $ARCH -shared -o $OUT/libtlbm.so $O/abi.o $O/fields.o $O/peer.o $O/step.o $O/tiler.o \
+nvcc $ARCH -shared -o $OUT/libtlbm.so $(ls $O/*.o | grep -v -E "step_f(32|64).o") \
     $OUT/step_f32.o $OUT/step_f64.o
 echo $OUT/libtlbm.so

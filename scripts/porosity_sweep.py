@@ -28,10 +28,10 @@ def hbm_gbs():
     return json.load(open(p))["hbm_gbs"] if os.path.exists(p) else 6650.0
 
 
-def time_case(name, geo, precision, steps, warmup, table):
+def time_case(name, geo, precision, steps, warmup, table, storage="blocks"):
     t0 = time.perf_counter()
     cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table,
-                           u_max_guard=0.0)
+                           u_max_guard=0.0, storage=storage)
     s = Solver(geo, cfg)
     setup = time.perf_counter() - t0
     s.step(warmup, check=False)
@@ -45,7 +45,8 @@ def time_case(name, geo, precision, steps, warmup, table):
     ms = e0.elapsed_time(e1) / steps
     b_node = 304 if precision == "f64" else 152
     mlups = s.n_fn / (ms / 1e3) / 1e6
-    rec = {"case": name, "precision": precision, "table": table, "dims": list(geo.shape),
+    rec = {"case": name, "precision": precision, "table": cfg.table.value, "storage": storage,
+           "dims": list(geo.shape),
            "porosity": geo.porosity(), "t_n": s.t_n, "n_fn": s.n_fn,
            "eta_t": s.n_fn / (64 * s.t_n), "ms_per_step": ms, "mlups": mlups,
            "bu": mlups * 1e6 * b_node / (hbm_gbs() * 1e9), "setup_s": setup, "steps": steps}
@@ -61,10 +62,11 @@ def main():
     p.add_argument("--n", type=int, default=256)
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--table", default="b200")
+    p.add_argument("--table", default=None, help="default: b200 (blocks), xyz (compact)")
     p.add_argument("--vessel", action="store_true")
     p.add_argument("--cavity", action="store_true")
     p.add_argument("--l2-fetch", type=int, default=-1)
+    p.add_argument("--storages", default="blocks", help="comma list of blocks,compact")
     a = p.parse_args()
     if a.l2_fetch >= 0:
         from paper_1611_02445_b200 import _native as nat
@@ -84,10 +86,11 @@ def main():
     if a.cavity:
         cases.append(("cavity64", workloads.cavity(64), 0.0))
     for name, geo, gen_s in cases:
-        for prec in a.precisions.split(","):
-            rec = time_case(name, geo, prec, a.steps, a.warmup, a.table)
-            rec["geometry_s"] = gen_s
-            print(json.dumps(rec), flush=True)
+        for storage in a.storages.split(","):
+            for prec in a.precisions.split(","):
+                rec = time_case(name, geo, prec, a.steps, a.warmup, a.table, storage)
+                rec["geometry_s"] = gen_s
+                print(json.dumps(rec), flush=True)
 
 
 if __name__ == "__main__":

@@ -15,7 +15,7 @@ from paper_1611_02445_b200 import workloads  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--n", type=int, default=256)
 p.add_argument("--precision", default="f64")
-p.add_argument("--table", default="b200")
+p.add_argument("--table", default=None, help="layout table (default: b200, xyz if compact)")
 p.add_argument("--steps", type=int, default=100)
 p.add_argument("--variants", default="full,prop,rw")
 p.add_argument("--geometry", default="channel", help="channel | channel_z | cavity | pack")
@@ -26,6 +26,7 @@ p.add_argument("--porosity", type=float, default=0.5)
 p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
 p.add_argument("--arith", default="reference", choices=["reference", "fma"])
 p.add_argument("--graph", action="store_true", help="replay captured CUDA graphs of steps")
+p.add_argument("--storage", default="blocks", choices=["blocks", "compact"])
 p.add_argument("--l2-fetch", type=int, default=-1,
                help="cudaLimitMaxL2FetchGranularity in bytes (0..128; -1 leaves the default)")
 a = p.parse_args()
@@ -41,7 +42,8 @@ elif a.geometry == "cavity":
 else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
-                          index64=a.index64, arithmetic=a.arith, perturb=not a.no_perturb)
+                          index64=a.index64, arithmetic=a.arith, perturb=not a.no_perturb,
+                          storage=a.storage)
 if a.no_perturb:
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04) if a.geometry == "channel_z" else (0.04, 0.0, 0.0))
 from paper_1611_02445_b200.solver import GRAPH_STEPS as solver_graph_steps  # noqa: E402
@@ -59,7 +61,8 @@ for v in a.variants.split(","):
     if v == "mrt" and "mrt" not in solvers:
         from paper_1611_02445_b200.solver import SimulationConfig, Solver
         cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision=a.precision,
-                               table=a.table, u_max_guard=0.0, arithmetic=a.arith)
+                               table=a.table, u_max_guard=0.0, arithmetic=a.arith,
+                               storage=a.storage)
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
         s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
@@ -75,6 +78,7 @@ for v in a.variants.split(","):
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
     print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
                       "arith": a.arith, "graph": a.graph, "l2_fetch": l2_fetch,
+                      "storage": a.storage,
                       "geometry": a.geometry, "n": a.n, "dims": list(geo.shape),
                       "field_gb": round(2 * s.t_n * 19 * 64 * n_d / 1e9, 2),
                       "precision": a.precision, "table": a.table, "variant": v,

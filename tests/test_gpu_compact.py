@@ -1,0 +1,122 @@
+"""GPU: compact tile storage (SimulationConfig(storage="compact"),
+csrc/compact.cu, csrc/step_compact.cuh).  The compact store keeps only the
+non-solid slots of every block; the arithmetic is the block-store kernel's,
+so every result is bit-identical to the paper's layout and to the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+from helpers import random_geometry
+from oracle import dense, numerics as nm
+from paper_1611_02445_b200 import _native as nat
+from paper_1611_02445_b200 import geometry, layout, slabs, solver
+from test_gpu_step import DTYPES, MODELS, compare, oracle_run, perturbed_eq
+
+pytestmark = pytest.mark.gpu
+def make(geo, m=MODELS["inc"], dt=np.float64, table=None, f0=None, storage="compact", **kw):
+    cfg = solver.SimulationConfig(fluid=m, tau=0.6, u_max_guard=0.0, table=table,
+                                  precision="f64" if dt == np.float64 else "f32",
+                                  storage=storage, **kw)
+    s = solver.Solver(geo, cfg)
+    if f0 is not None:
+        s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+    return s
+
+
+def test_store_size_and_canonical_roundtrip():
+    geo = geometry.generate_sphere_pack(24, 6, 0.4, seed=3, inlet_velocity=(0, 0, 0.01))
+    s = make(geo)
+    assert s.store.flat.numel() == 2 * 19 * s.n_fn < 2 * 19 * 64 * s.t_n
+    vals = np.random.default_rng(0).random((19, s.t_n, 64))
+    s.set_fields_canonical(vals)
+    got = s.fields_canonical()
+    mask = s.nonsolid_mask()
+    assert np.array_equal(got[:, mask], vals[:, mask])
+    assert np.array_equal(got[:, ~mask], np.broadcast_to(nm.W[:, None], (19, (~mask).sum())))
+
+
+def test_rejects_unsupported_configs():
+    assert solver.SimulationConfig(storage="compact").table is layout.LayoutTable.XYZ
+    for t in ("optimized", "b200"):
+        with pytest.raises(ValueError):
+            solver.SimulationConfig(storage="compact", table=t)
+    with pytest.raises(ValueError):
+        solver.SimulationConfig(storage="sparse")
+    geo = geometry.generate_channel("square", 8, axis=2, length=16, ends="periodic")
+    with pytest.raises(ValueError, match="block storage"):
+        slabs.VirtualSlabs(geo, 2, solver.SimulationConfig(storage="compact"))
+
+
+@pytest.mark.parametrize("dn", DTYPES)
+def test_cavity64_1000_steps_compact(c_oracle, dn):
+    dt = DTYPES[dn]
+    geo = geometry.generate_cavity3d(64)
+    m = MODELS["inc"]
+    s = make(geo, m, dt)
+    s.run(1000)
+    compare(s, oracle_run(c_oracle, geo, m, dt, dense.init_equilibrium(geo.shape, m, dt), 1000),
+            dt)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_geometries_compact(c_oracle, seed):
+    """Mixed solid / fluid / bounce-back / inlet / outlet geometries, both
+    dtypes and fluid models: bit-exact vs the oracle."""
+    rng = np.random.default_rng(1300 + seed)
+    shape = tuple(int(v) for v in rng.integers(5, 26, size=3))
+    t = random_geometry(rng, shape)
+    geo = geometry.Geometry(t, inlet_velocity=(0.0, 0.01, 0.02), outlet_density=1.0)
+    for dt in (np.float64, np.float32):
+        for m in MODELS.values():
+            f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), seed)
+            want = oracle_run(c_oracle, geo, m, dt, f0, 15)
+            s = make(geo, m, dt, None, f0)
+            s.step(15)
+            compare(s, want, dt)
+
+
+@pytest.mark.parametrize("kw", [{}, {"collision": "mrt"}, {"arithmetic": "fma"},
+                                {"collision": "mrt", "arithmetic": "fma"},
+                                {"fluid": "quasi-compressible", "precision": "f32"}])
+def test_compact_equals_blocks(kw):
+    """Same configuration, both storages, 70 steps (graph replay for the
+    compact one): identical canonical fields and macroscopic readout."""
+    geo = geometry.generate_sphere_pack(32, 8, 0.45, seed=6, inlet_velocity=(0, 0, 0.02))
+    runs = []
+    for storage in ("blocks", "compact"):
+        cfg = solver.SimulationConfig(tau=0.6, u_max_guard=0.0, storage=storage,
+                                      **({"fluid": "incompressible"} | kw))
+        s = solver.Solver(geo, cfg)
+        s.init_equilibrium(1.0, (0.0, 0.0, 0.01))
+        s.step(70, graph=(storage == "compact"))
+        mask = s.nonsolid_mask(device=True)
+        rho, u, _ = s.macroscopic(device=True)
+        runs.append((s.fields_canonical(device=True)[:, mask], rho[mask], u[:, mask]))
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("variant", [nat.PROPAGATION_ONLY, nat.READ_WRITE_ONLY])
+def test_ladder_variants_compact(variant):
+    geo = geometry.generate_sphere_pack(24, 6, 0.5, seed=2, inlet_velocity=(0, 0, 0.01))
+    f0 = perturbed_eq(geo.shape, MODELS["inc"], np.float64, seed=5)
+    runs = []
+    for storage in ("blocks", "compact"):
+        s = make(geo, f0=f0, storage=storage)
+        s.step(3, variant=variant)
+        runs.append(s.fields_canonical(device=True)[:, s.nonsolid_mask(device=True)])
+    assert torch.equal(runs[0], runs[1])
+
+
+def test_checkpoint_across_storages(tmp_path):
+    geo = geometry.generate_sphere_pack(24, 6, 0.5, seed=8, inlet_velocity=(0, 0, 0.02))
+    a = make(geo)
+    a.step(9)
+    a.save_checkpoint(tmp_path / "ck.npz")
+    a.step(11)
+    b = solver.Solver(geo, solver.SimulationConfig(u_max_guard=0.0, tau=0.6))
+    b.load_checkpoint(tmp_path / "ck.npz")
+    b.step(11)
+    m = b.nonsolid_mask(device=True)
+    assert torch.equal(a.fields_canonical(device=True)[:, m], b.fields_canonical(device=True)[:, m])
