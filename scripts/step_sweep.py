@@ -18,8 +18,10 @@ p.add_argument("--precision", default="f64")
 p.add_argument("--table", default=None, help="layout table (default: b200, xyz if compact)")
 p.add_argument("--steps", type=int, default=100)
 p.add_argument("--variants", default="full,prop,rw")
-p.add_argument("--geometry", default="channel", help="channel | channel_z | cavity | pack")
+p.add_argument("--geometry", default="channel",
+               help="channel | channel_z | duct_z | cavity | pack | vessel")
 p.add_argument("--length", type=int, default=None, help="channel_z length along z")
+p.add_argument("--dims", default="512,512,1024", help="vessel dims nx,ny,nz")
 p.add_argument("--no-perturb", action="store_true",
                help="uniform equilibrium start (no (t_n, 64) init temporaries; big domains)")
 p.add_argument("--porosity", type=float, default=0.5)
@@ -37,6 +39,8 @@ elif a.geometry == "channel_z":
 elif a.geometry == "duct_z":        # walled square duct along z (no periodic wrap)
     from paper_1611_02445_b200 import geometry as _g
     geo = _g.generate_channel("square", a.n, axis=2, length=a.length or a.n, ends="wall")
+elif a.geometry == "vessel":        # tortuous vessel tree (BASELINE configs 4 and 5)
+    geo = workloads.vessel_tree(tuple(int(v) for v in a.dims.split(",")))
 elif a.geometry == "cavity":
     geo = workloads.cavity(a.n)
 else:
@@ -80,7 +84,7 @@ for v in a.variants.split(","):
                       "arith": a.arith, "graph": a.graph, "l2_fetch": l2_fetch,
                       "storage": a.storage,
                       "geometry": a.geometry, "n": a.n, "dims": list(geo.shape),
-                      "field_gb": round(2 * s.t_n * 19 * 64 * n_d / 1e9, 2),
+                      "field_gb": round(s.store.flat.numel() * n_d / 1e9, 2),
                       "precision": a.precision, "table": a.table, "variant": v,
                       "ms": round(ms, 4), "mlups": round(mlups, 1), "gbs": round(gbs, 1),
                       "frac": round(gbs / 6533.5, 4), "n_fn": s.n_fn, "t_n": s.t_n}), flush=True)
