@@ -173,7 +173,7 @@ def build_parser():
         sp.add_argument("--layout", default=None, choices=["b200", "optimized", "xyz"],
                         help="default: b200 (blocks storage), xyz (compact)")
         sp.add_argument("--arith", default="reference", choices=["reference", "fma"])
-        sp.add_argument("--storage", default="blocks", choices=["blocks", "compact"])
+        sp.add_argument("--storage", default="blocks", choices=["blocks", "compact", "auto"])
 
     r = sub.add_parser("run")
     sim_args(r)

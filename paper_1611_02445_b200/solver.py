@@ -13,7 +13,9 @@ step semantics are restated in SURVEY Appendix A).  API:
                       stated 1e-12 tolerance; f64 only), and ``storage``:
                       "blocks" (default, the paper's 64-slot blocks) or
                       "compact" (only the non-solid slots of every block;
-                      less DRAM traffic on sparse geometries, single GPU).
+                      less DRAM traffic on sparse geometries, single GPU)
+                      or "auto" (compact for fp64 when the tile
+                      utilisation eta_t < AUTO_COMPACT_ETA, else blocks).
 ``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,
                       iteration, parity).
 ``Solver``            owns the device state; ``step(n)``, ``run(n)``,
@@ -62,22 +64,25 @@ class SimulationConfig:
     table: LayoutTable = None      # default: B200 (blocks storage), XYZ (compact)
     mrt_matrix: object = None      # optional explicit 19x19 operator (overrides rates)
     arithmetic: str = "reference"  # "reference" (bit-exact) | "fma"
-    storage: str = "blocks"        # "blocks" (the paper's 64-slot blocks) | "compact"
+    storage: str = "blocks"        # "blocks" (the paper's 64-slot blocks) | "compact" | "auto"
 
     def __post_init__(self):
         self.collision = CollisionModel(getattr(self.collision, "value", self.collision))
         self.fluid = FluidModel(getattr(self.fluid, "value", self.fluid))
-        if self.table is None:
+        if self.storage not in ("blocks", "compact", "auto"):
+            raise ValueError(f"unknown storage: {self.storage!r}")
+        if self.table is None and self.storage != "auto":
             self.table = LayoutTable.XYZ if self.storage == "compact" else LayoutTable.B200
-        self.table = LayoutTable(getattr(self.table, "value", self.table))
+        if self.table is not None:
+            self.table = LayoutTable(getattr(self.table, "value", self.table))
         if not float(self.tau) > 0.5:
             raise ValueError(f"relaxation time must exceed 0.5: {self.tau}")
         if self.precision not in ("f32", "f64"):
             raise ValueError(f"unknown precision: {self.precision!r}")
         if self.arithmetic not in ("reference", "fma"):
             raise ValueError(f"unknown arithmetic: {self.arithmetic!r}")
-        if self.storage not in ("blocks", "compact"):
-            raise ValueError(f"unknown storage: {self.storage!r}")
+        if self.storage == "auto" and self.table is not None:
+            raise ValueError("storage='auto' picks the layout table itself; leave table unset")
         if self.storage == "compact" and self.table is not LayoutTable.XYZ:
             raise ValueError("compact storage keeps blocks in XYZ order: table must be xyz")
         if self.arithmetic == "fma" and self.precision != "f64":
@@ -133,6 +138,8 @@ class Solver:
         self.device = self.tiling.device
         self.t_n = self.tiling.t_n
         self.n_fn = self.tiling.n_fn
+        if self.config.storage == "auto":
+            self.config = resolve_auto_storage(self.config, self.n_fn, self.t_n)
         if self.config.storage == "compact":
             self.store = CompactFieldStore(self.tiling, self.config.table, self.config.dtype)
         else:
@@ -503,6 +510,20 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
     if callable(outputs):
         outputs(solver)
     return solver.state, diagnostics
+
+
+# storage="auto": compact below this tile utilisation (fp64).  From the
+# porosity sweep (profiles/r1b_porosity_sweep_storage.jsonl): compact is
+# +2% at eta_t 0.866 (porosity 0.6), -1.5% at 0.904 (0.7), +21% at 0.658.
+AUTO_COMPACT_ETA = 0.88
+
+
+def resolve_auto_storage(config, n_fn, t_n):
+    """The concrete configuration storage="auto" stands for on a tiling."""
+    import dataclasses
+    eta = n_fn / (64.0 * t_n) if t_n else 1.0
+    compact = config.precision == "f64" and eta < AUTO_COMPACT_ETA
+    return dataclasses.replace(config, storage="compact" if compact else "blocks", table=None)
 
 
 CHECKPOINT_FORMAT = "tlbm-checkpoint-1"

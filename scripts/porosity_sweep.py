@@ -45,7 +45,8 @@ def time_case(name, geo, precision, steps, warmup, table, storage="blocks"):
     ms = e0.elapsed_time(e1) / steps
     b_node = 304 if precision == "f64" else 152
     mlups = s.n_fn / (ms / 1e3) / 1e6
-    rec = {"case": name, "precision": precision, "table": cfg.table.value, "storage": storage,
+    rec = {"case": name, "precision": precision, "table": s.config.table.value,
+           "storage": storage, "storage_used": s.config.storage,
            "dims": list(geo.shape),
            "porosity": geo.porosity(), "t_n": s.t_n, "n_fn": s.n_fn,
            "eta_t": s.n_fn / (64 * s.t_n), "ms_per_step": ms, "mlups": mlups,
@@ -66,7 +67,7 @@ def main():
     p.add_argument("--vessel", action="store_true")
     p.add_argument("--cavity", action="store_true")
     p.add_argument("--l2-fetch", type=int, default=-1)
-    p.add_argument("--storages", default="blocks", help="comma list of blocks,compact")
+    p.add_argument("--storages", default="blocks", help="comma list of blocks,compact,auto")
     a = p.parse_args()
     if a.l2_fetch >= 0:
         from paper_1611_02445_b200 import _native as nat

@@ -120,3 +120,11 @@ def test_checkpoint_across_storages(tmp_path):
     b.step(11)
     m = b.nonsolid_mask(device=True)
     assert torch.equal(a.fields_canonical(device=True)[:, m], b.fields_canonical(device=True)[:, m])
+
+
+def test_auto_storage_picks_by_tile_utilisation():
+    sparse = geometry.generate_sphere_pack(32, 8, 0.3, seed=1, inlet_velocity=(0, 0, 0.01))
+    dense = geometry.generate_channel("square", 16, axis=2, length=16, ends="periodic")
+    cfg = solver.SimulationConfig(storage="auto", u_max_guard=0.0)
+    assert solver.Solver(sparse, cfg).config.storage == "compact"
+    assert solver.Solver(dense, cfg).config.storage == "blocks"

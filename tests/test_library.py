@@ -120,3 +120,18 @@ def test_geometry_fingerprint_distinguishes_inputs():
     t = a.types.copy()
     t[3, 3, 3] = 0
     assert solver.geometry_fingerprint(a) != solver.geometry_fingerprint(geometry.Geometry(t))
+
+
+def test_auto_storage_resolution():
+    from paper_1611_02445_b200 import layout, solver
+    c = solver.SimulationConfig(storage="auto")
+    assert c.table is None
+    sparse = solver.resolve_auto_storage(c, n_fn=40 * 100, t_n=100)      # eta_t 0.625
+    dense = solver.resolve_auto_storage(c, n_fn=64 * 100, t_n=100)
+    assert (sparse.storage, sparse.table) == ("compact", layout.LayoutTable.XYZ)
+    assert (dense.storage, dense.table) == ("blocks", layout.LayoutTable.B200)
+    f32 = solver.resolve_auto_storage(solver.SimulationConfig(storage="auto", precision="f32"),
+                                      n_fn=40 * 100, t_n=100)
+    assert f32.storage == "blocks"
+    with pytest.raises(ValueError):
+        solver.SimulationConfig(storage="auto", table="xyz")
