@@ -146,6 +146,8 @@ class SlabSolver:
         self.interior = (self.bottom[1], self.top[0]) if len(own) > 2 else (self.top[0],
                                                                             self.top[0])
         self.n_fn_owned = int(s.tiling.counts[self.own[0]:self.own[1]].sum().item())
+        self._side = None
+        self._n_over = 0
         dt = s.store.tdtype
         dev = s.device
         nb = lambda r: torch.empty(max(r[1] - r[0], 0) * 80, dtype=dt, device=dev)  # noqa
@@ -175,6 +177,54 @@ class SlabSolver:
     def step_interior(self):
         self._launch(self.interior)
 
+    # -- interior / boundary overlap on two streams --------------------------
+    def step_overlapped(self, before=None, after=None, wait_events=()):
+        """One step with the interior tiles on the current stream and the
+        boundary layers on a high-priority side stream, so they run
+        concurrently (the boundary launches fill the interior's tail instead
+        of following it).  ``before`` / ``after`` run on the side stream
+        around the boundary launches (peer wait + arm / disarm + signal);
+        ``wait_events`` are extra events the side stream waits on first.
+
+        Ordering, step t: the interior waits for boundary t-1 (it reads the
+        boundary tiles t-1 wrote, and writes the copy boundary t-1 read); the
+        boundary waits for everything the current stream had before interior
+        t, i.e. interior t-1 (same reasons).  Interior t and boundary t read
+        the same copy and write disjoint tiles of the other."""
+        dev = self.solver.device
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=dev, priority=-1)
+            self._ev_pre = [torch.cuda.Event(), torch.cuda.Event()]
+            self._ev_bnd = [torch.cuda.Event(), torch.cuda.Event()]
+        main = torch.cuda.current_stream(dev)
+        t = self._n_over
+        if t > 0:
+            main.wait_event(self._ev_bnd[(t - 1) % 2])
+        self._ev_pre[t % 2].record(main)
+        self.step_interior()
+        with torch.cuda.stream(self._side):
+            self._side.wait_event(self._ev_pre[t % 2])
+            for ev in wait_events:
+                self._side.wait_event(ev)
+            if before is not None:
+                before()
+            self.step_boundary()
+            if after is not None:
+                after()
+            self._ev_bnd[t % 2].record(self._side)
+        self._n_over += 1
+
+    def last_boundary_event(self):
+        return self._ev_bnd[(self._n_over - 1) % 2] if self._n_over > 0 else None
+
+    def join(self):
+        """Make the current stream wait for the side stream's last boundary
+        launch (before any host read or non-overlapped launch)."""
+        if self._n_over > 0:
+            torch.cuda.current_stream(self.solver.device).wait_event(
+                self._ev_bnd[(self._n_over - 1) % 2])
+            self._n_over = 0
+
     def _halo(self, rng, up, pack, buf, copy):
         s = self.solver
         nat.call("tlbm_halo", nat.ptr(s.store.copy_tensor(copy)), s.code, s.table,
@@ -201,6 +251,7 @@ class SlabSolver:
         s.parity ^= 1
         s.iteration += 1
         if s.iteration - s._checked >= len(s.status) - 1:
+            self.join()
             s.check()
 
     def fields_owned(self):
@@ -460,17 +511,14 @@ class DistributedSlabRunner:
                 sl.finish()
                 continue
             if self.ipc is not None:
-                # interior first: it reads and writes only this rank's own
-                # tiles, so it needs no neighbour and covers any skew
-                # between ranks; then the wait, the boundary layers with the
-                # fused peer stores, and the signal right after them
+                # interior tiles on the main stream (own tiles only, no
+                # neighbour needed); on the high-priority side stream,
+                # concurrently: the neighbour wait, the boundary layers with
+                # the fused peer stores, and the signal right after them
                 it = sl.solver.iteration
-                sl.step_interior()
-                self.ipc.wait(it)
-                self.ipc.arm()
-                sl.step_boundary()
-                self.ipc.disarm()
-                self.ipc.signal(it + 1)
+                ipc = self.ipc
+                sl.step_overlapped(before=lambda: (ipc.wait(it), ipc.arm()),
+                                   after=lambda: (ipc.disarm(), ipc.signal(it + 1)))
                 sl.finish()
                 continue
             sl.step_boundary()
@@ -480,6 +528,7 @@ class DistributedSlabRunner:
             self.halo.wait(reqs)
             sl.unpack()
             sl.finish()
+        sl.join()
 
     def barrier(self):
         if self.halo is not None:
@@ -487,14 +536,20 @@ class DistributedSlabRunner:
 
 
 class VirtualSlabs:
-    """All slabs of a decomposition on ONE device, exchanged by device copies
-    -- exercises the partition, halo pack/unpack and ghost logic of the
-    multi-GPU path on a single GPU."""
+    """All slabs of a decomposition on ONE device -- exercises the partition,
+    halo and ghost logic of the multi-GPU path on a single GPU.
 
-    def __init__(self, geometry, world, config=None, device=None):
+    ``fused=False``: halos move by pack -> device copy -> unpack (the NCCL
+    path's data flow).  ``fused=True``: the boundary-layer launches store
+    their outgoing planes straight into the neighbour slab's ghost tiles,
+    the fused-halo kernels of the IPC path with device pointers in place of
+    peer mappings; slabs run one after another on one stream, so no step
+    counters are needed (scripts/halo_overhead.py times this path)."""
+
+    def __init__(self, geometry, world, config=None, device=None, fused=False):
         self.plan = SlabPlan(geometry, world)
         self.slabs = [SlabSolver(geometry, self.plan, r, config, device) for r in range(world)]
-
+        self.fused = bool(fused)
     def _exchange(self):
         for sl in self.slabs:
             r = sl.range
@@ -512,6 +567,22 @@ class VirtualSlabs:
 
     def step(self, n=1):
         for _ in range(int(n)):
+            if self.fused:
+                # each slab: interior on the main stream, boundary layers on
+                # its side stream after the neighbours' previous boundary
+                # launches (they read the ghost tiles this step writes and
+                # wrote the ghost tiles this step reads) -- the ordering the
+                # IPC path gets from the step counters
+                evs = [sl.last_boundary_event() for sl in self.slabs]
+                for sl in self.slabs:
+                    r = sl.range
+                    waits = [evs[k] for k in (r.lower, r.upper) if k >= 0 and evs[k] is not None]
+                    sl.step_overlapped(before=lambda sl=sl: self._arm(sl),
+                                       after=lambda sl=sl: self._disarm(sl),
+                                       wait_events=waits)
+                for sl in self.slabs:
+                    sl.finish()
+                continue
             for sl in self.slabs:
                 sl.step_boundary()
                 sl.pack()
@@ -520,6 +591,28 @@ class VirtualSlabs:
                 sl.step_interior()
                 sl.unpack()
                 sl.finish()
+        for sl in self.slabs:
+            sl.join()
+
+    @staticmethod
+    def _disarm(sl):
+        a = sl.solver._args
+        a.halo_up = a.halo_down = None
+
+    def _arm(self, sl):
+        """Point a slab's halo fields at its neighbours' ghost tiles of the
+        copy this step writes (IpcHalo.arm with device pointers)."""
+        a, r = sl.solver._args, sl.range
+        dst = 1 - sl.solver.parity
+        tile_bytes = 19 * 64 * sl.solver.store.flat.element_size()
+        if r.upper >= 0:
+            u = self.slabs[r.upper]
+            a.halo_up = u.solver.store.copy_tensor(dst).data_ptr() + u.ghost_lo[0] * tile_bytes
+            a.halo_up_begin, a.halo_up_end = sl.top
+        if r.lower >= 0:
+            lo = self.slabs[r.lower]
+            a.halo_down = lo.solver.store.copy_tensor(dst).data_ptr() + lo.ghost_hi[0] * tile_bytes
+            a.halo_down_begin, a.halo_down_end = sl.bottom
 
     def fields_owned(self):
         return torch.cat([sl.fields_owned() for sl in self.slabs], dim=1)

@@ -37,10 +37,11 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("world", [2, 3, 5])
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("dt", [np.float64, np.float32])
-def test_virtual_slabs_bit_identical(name, world, dt):
+def test_virtual_slabs_bit_identical(name, world, dt, fused):
     geo = CASES[name]()
     prec = "f64" if dt == np.float64 else "f32"
     cfg = solver.SimulationConfig(precision=prec, u_max_guard=0.0)
@@ -51,7 +52,7 @@ def test_virtual_slabs_bit_identical(name, world, dt):
     ref.step(steps)
     want = ref.to_dense(ref.fields_canonical(device=True))
 
-    vs = slabs.VirtualSlabs(geo, world, cfg)
+    vs = slabs.VirtualSlabs(geo, world, cfg, fused=fused)
     nz = geo.shape[2]
     for sl in vs.slabs:
         s = sl.solver
