@@ -1,0 +1,64 @@
+"""GPU property test (SPEC acceptance 6, hypothesis-driven): on random
+geometries -- shape, solid fraction, bounce-back / inlet / outlet faces,
+periodic axes -- and random solver configurations (dtype, fluid model,
+layout table, storage, collision model, arithmetic, CUDA-graph replay), the
+fused step equals the CPU oracle bit-exactly (reference arithmetic) or
+within the stated tolerance (FMA arithmetic)."""
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings, strategies as st
+
+from helpers import random_geometry
+from oracle import dense, numerics as nm
+from paper_1611_02445_b200 import geometry, solver
+from test_gpu_step import compare, oracle_run, perturbed_eq
+
+pytestmark = pytest.mark.gpu
+
+
+@st.composite
+def cases(draw):
+    per = draw(st.tuples(st.booleans(), st.booleans(), st.booleans()))
+    shape = tuple(draw(st.sampled_from([4, 8, 12])) if p else draw(st.integers(3, 19))
+                  for p in per)
+    seed = draw(st.integers(0, 2 ** 31 - 1))
+    prec = draw(st.sampled_from(["f64", "f32"]))
+    fluid = draw(st.sampled_from(["incompressible", "quasi-compressible"]))
+    storage = draw(st.sampled_from(["blocks", "compact"]))
+    table = draw(st.sampled_from(["b200", "optimized", "xyz"])) if storage == "blocks" else "xyz"
+    coll = draw(st.sampled_from(["lbgk", "mrt"]))
+    arith = draw(st.sampled_from(["reference", "fma"])) if prec == "f64" else "reference"
+    steps = draw(st.integers(1, 12))
+    graph = draw(st.booleans())
+    return per, shape, seed, prec, fluid, storage, table, coll, arith, steps, graph
+
+
+@settings(max_examples=300, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(case=cases())
+def test_step_matches_oracle(c_oracle, case):
+    per, shape, seed, prec, fluid, storage, table, coll, arith, steps, graph = case
+    rng = np.random.default_rng(seed)
+    t = random_geometry(rng, shape, periodic=per)
+    geo = geometry.Geometry(t, inlet_velocity=(0.0, 0.01, 0.02), outlet_density=1.0,
+                            periodic=per)
+    dt = np.float64 if prec == "f64" else np.float32
+    op = solver.SimulationConfig(collision="mrt").mrt_operator if coll == "mrt" else None
+    cfg = solver.SimulationConfig(collision=coll, fluid=fluid, tau=0.6, precision=prec,
+                                  table=table, storage=storage, arithmetic=arith,
+                                  u_max_guard=0.0, mrt_matrix=op)
+    m = cfg.fluid
+    f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), seed % 1000)
+    want = oracle_run(c_oracle, geo, m, dt, f0, steps, mrt_operator=op)
+    s = solver.Solver(geo, cfg)
+    s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+    if graph:
+        solver.GRAPH_STEPS, saved = 2, solver.GRAPH_STEPS   # small graphs: exercise replay
+        try:
+            s.step(steps, graph=True)
+        finally:
+            solver.GRAPH_STEPS = saved
+    else:
+        s.step(steps)
+    compare(s, want, dt, exact=(arith == "reference"))
