@@ -7,6 +7,8 @@ set -u
 TAG=${1:-r1}
 O=gpurun_out/$TAG
 mkdir -p $O
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
 python bench.py > $O/bench.json 2> $O/bench.err
 python bench.py --precision f32 --no-cpu > $O/bench_f32.json 2>> $O/bench.err
 python bench.py --arith fma --no-cpu > $O/bench_fma.json 2>> $O/bench.err
@@ -16,7 +18,9 @@ python scripts/step_sweep.py --variants full,mrt --arith fma > $O/ladder_f64_fma
 python scripts/step_sweep.py --variants rw,prop,full,mrt --precision f32 > $O/ladder_f32.jsonl 2>/dev/null
 python scripts/step_sweep.py --geometry cavity --n 64 --variants full --steps 1000 > $O/cavity64.jsonl 2>/dev/null
 python scripts/step_sweep.py --geometry cavity --n 64 --variants full --steps 1000 --precision f32 >> $O/cavity64.jsonl 2>/dev/null
-python scripts/porosity_sweep.py --vessel --cavity > $O/sweep.jsonl 2> $O/sweep.err
+python scripts/porosity_sweep.py --vessel --cavity --storages blocks,compact > $O/sweep.jsonl 2> $O/sweep.err
+python scripts/halo_overhead.py --ranks 2,4,8 --steps 60 > $O/halo_overhead.jsonl 2>/dev/null
+python scripts/step_sweep.py --geometry cavity --n 64 --variants full --steps 1280 --graph >> $O/cavity64.jsonl 2>/dev/null
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches.csv \
     python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 for p in f64 f32; do
@@ -28,10 +32,14 @@ ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6
 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
     -o $O/prof_step_mrt_fma python scripts/step_sweep.py --variants mrt --steps 2 --arith fma > /dev/null 2>&1
 for p in 0.2 0.5 0.9; do
+  for st in blocks compact; do
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_p$p.csv \
-      python scripts/porosity_sweep.py --porosities $p --precisions f64 --steps 3 --warmup 5 > /dev/null 2>&1
+      -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_${st}_p$p.csv \
+      python scripts/porosity_sweep.py --porosities $p --precisions f64 --storages $st --steps 3 --warmup 5 > /dev/null 2>&1
+  done
 done
+ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5 -c 1 \
+    -o $O/prof_step_compact_p02 python scripts/porosity_sweep.py --porosities 0.2 --precisions f64 --storages compact --steps 3 --warmup 5 > /dev/null 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_vessel.csv \
     python scripts/porosity_sweep.py --porosities "" --vessel --precisions f64 --steps 3 --warmup 5 > /dev/null 2>&1

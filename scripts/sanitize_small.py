@@ -26,9 +26,23 @@ for coll in ("lbgk", "mrt"):
         s.step(2)
     s = solver.Solver(geo, solver.SimulationConfig(collision=coll, arithmetic="fma"))
     s.step(2)
-vs = slabs.VirtualSlabs(geometry.generate_channel("square", 12, axis=2, length=24,
-                                                  ends="periodic"), 3)
-vs.step(3)
+chan = geometry.generate_channel("square", 12, axis=2, length=24, ends="periodic")
+for fused in (False, True):
+    vs = slabs.VirtualSlabs(chan, 3, fused=fused)
+    vs.step(3)
+for prec in ("f64", "f32"):
+    s = solver.Solver(geo, solver.SimulationConfig(precision=prec, storage="compact"))
+    s.step(2)
+    s.step(1, variant=nat.PROPAGATION_ONLY)
+    s.step(1, variant=nat.READ_WRITE_ONLY)
+    s.macroscopic()
+    s.fields_canonical()
+s = solver.Solver(geo, solver.SimulationConfig(collision="mrt", storage="compact",
+                                               arithmetic="fma"))
+s.step(2)
+solver.GRAPH_STEPS = 4
+s = solver.Solver(geo, solver.SimulationConfig())
+s.step(9, graph=True)
 f = np.random.default_rng(0).random((19, 10))
 collision.collide_lbgk("incompressible", f, 0.7)
 print("sanitize run ok")
