@@ -70,11 +70,17 @@ constexpr int min_blocks_compact() {
            (2 * compact_tiles_per_cta<T>());
 }
 
-template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA>
+// OFF32: every element offset of a copy fits 32 bits (19 * n_fn < 2^32, i.e.
+// up to 226 M fluid nodes): neighbour block starts are staged as 32-bit
+// offsets from the copy start and each pull is one 32-bit add chain plus one
+// IMAD.WIDE.U32 from a single base -- fewer live registers than a 64-bit
+// pointer per pull.  Otherwise 64-bit block pointers are staged.
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32>
 __global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT>())
 step_kernel_compact(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
-    __shared__ const T *s_src[TPC][NBR];
+    __shared__ const T *s_src[OFF32 ? 1 : TPC][NBR];
+    __shared__ unsigned s_off[OFF32 ? TPC : 1][NBR];
     __shared__ int s_nf[TPC][NBR];
     __shared__ __align__(16) unsigned char s_rank[TPC][NBR][64];
     const int ti = threadIdx.x >> 6;
@@ -93,7 +99,8 @@ step_kernel_compact(const StepParams<T, MRT> p) {
         if (t < p.tile_end) nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1)
                                                                   : p.nbr[t * NBR + k];
         const long long tt = nb >= 0 ? nb : (t < p.tile_end ? t : p.tile_begin);
-        s_src[i / NBR][k] = p.src + p.cbase[tt];
+        if (OFF32) s_off[OFF32 ? i / NBR : 0][k] = (unsigned)p.cbase[tt];
+        else s_src[OFF32 ? 0 : i / NBR][k] = p.src + p.cbase[tt];
         s_nf[i / NBR][k] = p.cnf[tt];
         const uint4 *r = reinterpret_cast<const uint4 *>(p.crank + tt * 64);
         uint4 *d = reinterpret_cast<uint4 *>(&s_rank[i / NBR][k][0]);
@@ -104,14 +111,20 @@ step_kernel_compact(const StepParams<T, MRT> p) {
 
     uint32_t status = 0;
     if (meta & META_ACTIVE) {
-        const T *own_src = s_src[ti][13];
+        const T *base0 = opaque(p.src);
+        const T *own_src = OFF32 ? base0 + s_off[OFF32 ? ti : 0][13]
+                                 : s_src[OFF32 ? 0 : ti][13];
         const int nf_own = s_nf[ti][13];
         const int rank_own = s_rank[ti][13][j];
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
-                g[q] = load_ro(own_src + (q * nf_own + rank_own));
+                if (OFF32)
+                    g[q] = load_ro(base0 + (s_off[OFF32 ? ti : 0][13] +
+                                            (unsigned)(q * nf_own + rank_own)));
+                else
+                    g[q] = load_ro(own_src + (q * nf_own + rank_own));
                 continue;
             }
             // w = 64 * (source tile entry) + source slot
@@ -120,7 +133,11 @@ step_kernel_compact(const StepParams<T, MRT> p) {
             const int k = link ? (int)(w >> 6) : 13;
             const int rank = link ? (int)(&s_rank[ti][0][0])[w] : rank_own;
             const int blk = link ? q : opp(q);
-            g[q] = load_ro(s_src[ti][k] + (blk * s_nf[ti][k] + rank));
+            if (OFF32)
+                g[q] = load_ro(base0 + (s_off[OFF32 ? ti : 0][k] +
+                                        (unsigned)(blk * s_nf[ti][k] + rank)));
+            else
+                g[q] = load_ro(s_src[OFF32 ? 0 : ti][k] + (blk * s_nf[ti][k] + rank));
         }
 
         if (VARIANT == TLBM_FULL) {

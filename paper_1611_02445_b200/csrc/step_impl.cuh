@@ -397,8 +397,12 @@ int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int TPC = compact_tiles_per_cta<T>();
-    step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA>
-        <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+    if (a->rel32)       // for compact storage: 19 * n_fn < 2^32 (solver.py)
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true>
+            <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+    else
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false>
+            <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel_compact");
 }
 

@@ -167,6 +167,9 @@ class Solver:
         a.rel32 = int(self.tiling.rel32 and not index64)
         a.arith = nat.ARITH_FMA if self.config.arithmetic == "fma" else nat.ARITH_REFERENCE
         if self.config.storage == "compact":
+            # compact storage: rel32 means every element offset of a copy
+            # fits 32 bits (the kernel's OFF32 path)
+            a.rel32 = int(Q * self.n_fn < 2 ** 32 and not index64)
             a.cbase = self.store.base.data_ptr()
             a.cnf = self.store.nf.data_ptr()
             a.crank = self.store.rank.data_ptr()

@@ -43,6 +43,13 @@ ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:step_kernel -s 5 -c 1 --csv --log-file $O/ncu_sparse_vessel.csv \
     python scripts/porosity_sweep.py --porosities "" --vessel --precisions f64 --steps 3 --warmup 5 > /dev/null 2>&1
+# gpurun copies back at most 64 MiB: keep text/CSV exports of every full
+# capture and only the fp64 step report itself
+for r in $O/prof_step_*.ncu-rep; do
+  ncu -i $r --page details > ${r%.ncu-rep}_details.txt 2>&1
+  ncu -i $r --page raw --csv > ${r%.ncu-rep}_raw.csv 2>&1
+  [ "$r" = "$O/prof_step_f64.ncu-rep" ] || rm -f $r
+done
 timeout 900 compute-sanitizer --tool memcheck python scripts/sanitize_small.py > $O/memcheck.txt 2>&1
 timeout 900 compute-sanitizer --tool racecheck python scripts/sanitize_small.py > $O/racecheck.txt 2>&1
 tail -2 $O/memcheck.txt $O/racecheck.txt
