@@ -28,14 +28,15 @@
 namespace tlbm {
 namespace step_detail {
 
-// occupancy of the compact kernel (resident warps per SM): the rank
-// arithmetic needs more registers than the block-store kernel, so fp32 runs
-// at 32 warps/SM (64 registers; at 64 warps it spilled 240 bytes)
+// occupancy of the compact kernel (resident warps per SM): fp64 32 (64
+// registers); fp32 48 (40 registers, no spills with OFF32 addressing;
+// measured 23.4 / 28.0 / 32.5 GLUPS at porosity 0.2 / 0.5 / 1.0 vs 21.3 /
+// 25.6 / 28.0 at 32 warps, and the same at 64 warps with an 8-byte spill)
 #ifndef TLBM_WARPS_COMPACT
 #define TLBM_WARPS_COMPACT 32
 #endif
 #ifndef TLBM_WARPS_COMPACT_F32
-#define TLBM_WARPS_COMPACT_F32 32
+#define TLBM_WARPS_COMPACT_F32 48
 #endif
 // per (q, j): 64 * (neighbour-row entry of the source tile) + source slot
 struct CompactPull {
