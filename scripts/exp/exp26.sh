@@ -1,0 +1,10 @@
+# compact OFF32 path: fp32 occupancy variants (tuning; stdout only)
+timeout 900 python -m pytest tests/test_gpu_compact.py -q -x 2>&1 | tail -1
+for v in base c64 c48; do
+  if [ $v = base ]; then L=paper_1611_02445_b200/lib/libtlbm.so; else L=build/variants/$v/libtlbm.so; fi
+  TLBM_LIB=$L timeout 900 python scripts/porosity_sweep.py --porosities 0.2,0.5,1.0 --storages compact --precisions f32,f64 --steps 30 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('{'): d=json.loads(l); print('$v', d['case'], d['precision'], d['storage'], round(d['mlups']), round(d['bu'],3))
+    else: print(l.strip())"
+done

@@ -1,6 +1,7 @@
 """Summarise an ncu report (--set full) of the step kernel into JSON.
 
     python scripts/ncu_summary.py gpurun_out/r1b/prof_step.ncu-rep [n_fn] > out.json
+    python scripts/ncu_summary.py gpurun_out/r1c/prof_step_f32_raw.csv [n_fn] > out.json
 
 Reads `ncu -i --page raw --csv`; reports duration, DRAM bytes (read/write)
 per launch, throughput, L1/L2 sector counts and hit rates, occupancy and
@@ -40,8 +41,11 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12,
 def main():
     rep = sys.argv[1]
     n_fn = int(sys.argv[2]) if len(sys.argv) > 2 else None
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if rep.endswith(".csv"):           # a `--page raw --csv` export made on the GPU box
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     out = []
