@@ -10,9 +10,9 @@ python bench.py ${BENCH_ARGS:-} > $OUT/bench.json 2> $OUT/bench.err
 tail -c 3000 $OUT/bench.err
 cat $OUT/bench.json
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv \
-    --log-file $OUT/launches.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu \
+    --log-file $OUT/launches.csv python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-sweep \
     > $OUT/ncu_launch_run.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
-    -o $OUT/prof_step python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu \
+    -o $OUT/prof_step python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --no-sweep \
     > $OUT/ncu_full_run.log 2>&1
 ls -la $OUT

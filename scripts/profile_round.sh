@@ -10,8 +10,8 @@ mkdir -p $O
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
 python bench.py > $O/bench.json 2> $O/bench.err
-python bench.py --precision f32 --no-cpu > $O/bench_f32.json 2>> $O/bench.err
-python bench.py --arith fma --no-cpu > $O/bench_fma.json 2>> $O/bench.err
+python bench.py --precision f32 --no-cpu --no-sweep > $O/bench_f32.json 2>> $O/bench.err
+python bench.py --arith fma --no-cpu --no-sweep > $O/bench_fma.json 2>> $O/bench.err
 python bench.py --impl reference > $O/bench_ref.json 2>> $O/bench.err
 python scripts/step_sweep.py --variants rw,prop,full,mrt > $O/ladder_f64.jsonl 2>/dev/null
 python scripts/step_sweep.py --variants full,mrt --arith fma > $O/ladder_f64_fma.jsonl 2>/dev/null
@@ -22,10 +22,10 @@ python scripts/porosity_sweep.py --vessel --cavity --storages blocks,compact > $
 python scripts/halo_overhead.py --ranks 2,4,8 --steps 60 > $O/halo_overhead.jsonl 2>/dev/null
 python scripts/step_sweep.py --geometry cavity --n 64 --variants full --steps 1280 --graph >> $O/cavity64.jsonl 2>/dev/null
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches.csv \
-    python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+    python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-sweep > /dev/null 2>&1
 for p in f64 f32; do
   ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
-      -o $O/prof_step_$p python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --precision $p > /dev/null 2>&1
+      -o $O/prof_step_$p python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu --no-sweep --precision $p > /dev/null 2>&1
 done
 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 6 -c 1 \
     -o $O/prof_step_mrt python scripts/step_sweep.py --variants mrt --steps 2 > /dev/null 2>&1
