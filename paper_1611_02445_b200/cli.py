@@ -106,22 +106,14 @@ def cmd_bench(args):
 
 
 def cmd_tile_stats(args):
-    from fractions import Fraction
-
-    from . import geometry as g
     from . import tiling
     if args.channel:
         shape, d = args.channel.split(":")
+        rows, mean = tiling.channel_tiling_sweep(shape, int(d))
         print("off1,off2,eta_t")
-        etas = []
-        for o1 in range(4):
-            for o2 in range(4):
-                geo = g.generate_channel(shape, int(d), axis=0, offsets=(o1, o2), length=4)
-                grid = tiling.build_tiling(geo)
-                eta = Fraction(geo.nonsolid_count(), grid.t_n * 64)
-                etas.append(eta)
-                print(f"{o1},{o2},{float(eta)}")
-        print(f"mean,,{float(sum(etas) / len(etas))}")
+        for (o1, o2), eta in rows:
+            print(f"{o1},{o2},{float(eta)}")
+        print(f"mean,,{float(mean)}")
         return EXIT_OK
     geo = parse_geometry(args.geometry)
     grid = tiling.build_tiling(geo)

@@ -199,3 +199,39 @@ def overhead_memory(eta_t, q=19, n_d=8, n_t=1):
     if q <= 0 or n_d <= 0 or n_t < 0:
         raise ValueError("q and n_d must be positive, n_t non-negative")
     return (2.0 * q * n_d + n_t) / (eta_t * q * n_d) - 1.0, (2.0 - eta_t) / eta_t
+
+
+def channel_tiling_sweep(shape, d, axis=0, a=4):
+    """Tile utilisation of the 16 transverse placements (off1, off2) of a
+    straight channel (tiling.py:178-194): the cross-section repeats along the
+    axis, so one a-long slab per placement gives the infinite channel's
+    eta_t.  Returns ([((off1, off2), Fraction eta_t)], Fraction mean)."""
+    from fractions import Fraction
+
+    from .geometry import generate_channel
+    if a != TILE:
+        raise ValueError(f"only the solver tile edge {TILE} is supported, got {a}")
+    out = []
+    for off1, off2 in ((i, j) for i in range(a) for j in range(a)):
+        g = generate_channel(shape, d, axis=axis, offsets=(off1, off2), length=a)
+        grid = build_tiling(g, a)
+        out.append(((off1, off2), Fraction(g.nonsolid_count(), grid.t_n * a ** 3)))
+    return out, sum(e for _, e in out) / len(out)
+
+
+def bu_propagation_estimate(eta_f, eta_e):
+    """The paper's empirical bandwidth-utilisation fit of the gather
+    (tiling.py:197-216; fitted on one GPU, for comparison only):
+    0.92 - eta_f/14.28 - eta_e/25.74 + 0.00104/(2.9 - eta_f) + 0.0023/(2.81 - eta_e).
+    Raises at the fit's poles eta_f = 2.9, eta_e = 2.81."""
+    for v, pole, name in ((eta_f, 2.9, "eta_f"), (eta_e, 2.81, "eta_e")):
+        if v == pole:
+            raise ValueError(f"{name} = {pole} is a singularity of the fit")
+    return (0.92 - eta_f / 14.28 - eta_e / 25.74
+            + 0.00104 / (2.9 - eta_f) + 0.0023 / (2.81 - eta_e))
+
+
+def edge_face_plane_residual(eta_f, eta_e):
+    """eta_e - (1.85 eta_f - 2.56): distance from the paper's coarse
+    edge/face relation (tiling.py:219-221)."""
+    return eta_e - (1.85 * eta_f - 2.56)

@@ -94,3 +94,17 @@ def test_poiseuille_duct():
     err = np.linalg.norm(sim_n - ref_n) / np.linalg.norm(ref_n)
     print(f"poiseuille duct: {diag['iterations']} steps, rel L2 error {err:.4f}")
     assert err <= 0.02
+
+
+def test_acceptance4_channel_tiling_sweep():
+    """SPEC acceptance 4: square d = 8 -> {1 x1, 2/3 x6, 4/9 x9},
+    mean 9/16; circle d = 8 -> exactly {5/12, 15/32, 5/8, 15/16}."""
+    from fractions import Fraction
+    from paper_1611_02445_b200 import tiling
+    rows, mean = tiling.channel_tiling_sweep("square", 8)
+    etas = sorted(e for _, e in rows)
+    assert etas.count(Fraction(1)) == 1 and etas.count(Fraction(2, 3)) == 6
+    assert etas.count(Fraction(4, 9)) == 9 and mean == Fraction(9, 16)
+    rows, _ = tiling.channel_tiling_sweep("circle", 8)
+    assert {e for _, e in rows} == {Fraction(5, 12), Fraction(15, 32), Fraction(5, 8),
+                                    Fraction(15, 16)}

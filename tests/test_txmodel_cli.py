@@ -69,3 +69,23 @@ def test_vtk_writer_format_and_determinism():
     assert float(lines[first + 1]) == rho[1, 0, 0]          # x fastest
     vec = lines.index("VECTORS velocity double") + 1
     assert [float(v) for v in lines[vec].split()] == list(u[:, 0, 0, 0])
+
+
+def test_acceptance5_tiling_analytics():
+    """SPEC acceptance 5 and the BU_p pin."""
+    from paper_1611_02445_b200 import tiling
+    assert abs(tiling.overhead_generic(0.83) - 0.2048) < 1e-4
+    exact, approx = tiling.overhead_memory(1, 19, 8, 1)
+    assert abs(exact - 1.00658) < 1e-5 and approx == 1.0
+    assert tiling.overhead_memory(0.5, n_t=0)[0] == 3.0
+    assert abs(tiling.bu_propagation_estimate(0, 0) - 0.9212) < 1e-4
+    assert tiling.edge_face_plane_residual(2.0, 1.14) == pytest.approx(0.0)
+    with pytest.raises(ValueError):
+        tiling.bu_propagation_estimate(2.9, 0)
+
+
+def test_tiling_analytics_match_reference(reference):
+    from paper_1611_02445_b200 import tiling
+    for ef, ee in ((0.0, 0.0), (1.3, 0.7), (2.5, 2.2)):
+        assert tiling.bu_propagation_estimate(ef, ee) == reference.tiling.bu_propagation_estimate(ef, ee)
+        assert tiling.edge_face_plane_residual(ef, ee) == reference.tiling.edge_face_plane_residual(ef, ee)
