@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _native as nat
-from .lattice import OPPOSITE, Q
+from .lattice import E_VECTORS, OPPOSITE, Q, WEIGHTS  # noqa: F401 (reference namespace)
 
 
 class FluidModel(enum.Enum):
@@ -191,6 +191,33 @@ def mrt_operator(rates, dtype=np.float64):
         raise ValueError(f"expected 19 moment rates, got shape {rates.shape}")
     m = MOMENT_MATRIX.astype(np.float64)
     return (moment_matrix_inverse() @ (rates[:, None] * m)).astype(dtype)
+
+
+def apply_operator(op, delta):
+    """A 19x19 operator applied to (19, ...) data as 19 fixed-order row
+    accumulations that skip exact-zero coefficients (collision.py:216-231),
+    on the GPU.  Each term is computed as numpy computes ``acc += c *
+    delta[j]`` with ``c`` an element of ``op``: in the promoted type of
+    (op, delta), then stored in delta's dtype -- bit-identical to the
+    reference for float32 and float64 data."""
+    opa = np.asarray(op)
+    if opa.shape != (Q, Q):
+        raise ValueError(f"operator must be 19x19, got {opa.shape}")
+    dt, as_np = _to_device(delta)
+    if dt.shape[0] != Q:
+        raise ValueError(f"expected (19, ...) data, got {tuple(dt.shape)}")
+    wide = torch.float64 if (opa.dtype == np.float64 or dt.dtype == torch.float64) \
+        else torch.float32
+    out = torch.empty_like(dt)
+    dw = dt.to(wide)
+    for i in range(Q):
+        acc = torch.zeros_like(dt[0])
+        for j in range(Q):
+            c = opa[i, j]
+            if c != 0.0:
+                acc = (acc.to(wide) + float(c) * dw[j]).to(dt.dtype)
+        out[i] = acc
+    return _back(out, as_np)
 
 
 def collide_mrt(model, f, rates=None, operator=None):

@@ -34,6 +34,26 @@ def flop_per_byte(flop_count, bytes_per_node):
     return flop_count / bytes_per_node
 
 
+class PerfModel:
+    """Bandwidth-bound cost model (txmodel.py:32-45): per-node byte minima."""
+
+    def __init__(self, q=19, n_d=8, n_t=1, segment_bytes=SEGMENT_BYTES):
+        self.q, self.n_d, self.n_t, self.segment_bytes = q, n_d, n_t, segment_bytes
+
+    def __repr__(self):
+        return (f"PerfModel(q={self.q}, n_d={self.n_d}, n_t={self.n_t}, "
+                f"segment_bytes={self.segment_bytes})")
+
+    def __eq__(self, other):
+        return isinstance(other, PerfModel) and vars(self) == vars(other)
+
+    def m_node(self):
+        return m_node(self.q, self.n_d)
+
+    def b_node(self):
+        return b_node(self.q, self.n_d)
+
+
 def metadata_bytes(t_n):
     """Bytes of per-tile metadata one step reads: node words + neighbour row."""
     return t_n * (64 * 4 + 27 * 4)
@@ -51,6 +71,7 @@ import numpy as _np
 
 from . import lattice as _lat
 from . import layout as _lay
+from .lattice import TILE_X, TILE_Y, TILE_Z  # noqa: F401,E402 (reference namespace)
 
 
 @_dataclass

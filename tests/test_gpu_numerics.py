@@ -116,3 +116,28 @@ def test_mrt_setup_matches_oracle(golden):
     assert np.array_equal(collision.default_mrt_rates(0.6), g["mrt_rates_0.6"])
     assert np.allclose(collision.mrt_operator(collision.default_mrt_rates(0.6)),
                        g["mrt_op_0.6"], rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("dn", ["f64", "f32"])
+def test_apply_operator_golden(golden, dn):
+    """collision.apply_operator == the reference's fixed-order, zero-skipping
+    accumulation (collision.py:216-231), bit for bit (numpy reference run in
+    the test on the same inputs)."""
+    import numpy as np
+    from paper_1611_02445_b200 import collision
+    dt = np.float64 if dn == "f64" else np.float32
+    rng = np.random.default_rng(4)
+    op = golden("lattice")["mrt_op_0.6"].copy()
+    op[3, 5] = 0.0                                   # exercise the zero skip
+    for op_dt in (np.float64, dt):
+        opx = op.astype(op_dt)
+        d = (rng.standard_normal((19, 7, 5)) * 1e-3).astype(dt)
+        want = np.empty_like(d)
+        for i in range(19):
+            acc = np.zeros_like(d[0])
+            for j in range(19):
+                if opx[i, j] != 0.0:
+                    acc += opx[i, j] * d[j]
+            want[i] = acc
+        got = collision.apply_operator(opx, d)
+        assert got.dtype == d.dtype and np.array_equal(got, want)

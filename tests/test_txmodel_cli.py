@@ -89,3 +89,9 @@ def test_tiling_analytics_match_reference(reference):
     for ef, ee in ((0.0, 0.0), (1.3, 0.7), (2.5, 2.2)):
         assert tiling.bu_propagation_estimate(ef, ee) == reference.tiling.bu_propagation_estimate(ef, ee)
         assert tiling.edge_face_plane_residual(ef, ee) == reference.tiling.edge_face_plane_residual(ef, ee)
+
+
+def test_perf_model_matches_reference(reference):
+    for kw in ({}, {"n_d": 4}, {"q": 27, "n_d": 8, "n_t": 2}):
+        ours, ref = txmodel.PerfModel(**kw), reference.txmodel.PerfModel(**kw)
+        assert (ours.m_node(), ours.b_node()) == (ref.m_node(), ref.b_node())
