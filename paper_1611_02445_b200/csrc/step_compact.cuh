@@ -96,9 +96,12 @@ step_kernel_compact(const StepParams<T, MRT> p) {
     for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
         const long long t = tile0 + i / NBR;
         const int k = i % NBR;
+        // no D3Q19 pull reads one of the 8 corner neighbours: not staged
+        if (k == 0 || k == 2 || k == 6 || k == 8 || k == 18 || k == 20 || k == 24 || k == 26)
+            continue;
         long long nb = -1;
-        if (t < p.tile_end) nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1)
-                                                                  : p.nbr[t * NBR + k];
+        if (t < p.tile_end)
+            nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1) : p.nbr[t * NBR + k];
         const long long tt = nb >= 0 ? nb : (t < p.tile_end ? t : p.tile_begin);
         if (OFF32) s_off[OFF32 ? i / NBR : 0][k] = (unsigned)p.cbase[tt];
         else s_src[OFF32 ? 0 : i / NBR][k] = p.src + p.cbase[tt];
