@@ -130,6 +130,9 @@ class SlabSolver:
         self.plan, self.rank = plan, rank
         self.range = plan.ranges[rank]
         self.local_geometry = plan.local_geometry(geometry, rank)
+        if config is not None and config.storage == "auto":
+            import dataclasses
+            config = dataclasses.replace(config, storage="blocks", table=None)
         if config is not None and config.storage != "blocks":
             raise ValueError("slab decomposition needs the block storage (storage='blocks'): "
                              "halo pack/unpack and the fused peer stores address 64-slot "
