@@ -108,3 +108,30 @@ def test_acceptance4_channel_tiling_sweep():
     rows, _ = tiling.channel_tiling_sweep("circle", 8)
     assert {e for _, e in rows} == {Fraction(5, 12), Fraction(15, 32), Fraction(5, 8),
                                     Fraction(15, 16)}
+
+
+@pytest.mark.parametrize("transport", ["ipc", "gloo"])
+def test_bench_two_ranks_on_one_gpu(transport):
+    """The N > 1 bench path (torchrun, fused IPC halo or host-staged gloo
+    halo) runs end to end with both ranks on cuda:0 and prints one line."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "6",
+                        "--warmup", "3", "--edge", "64", "--transport", transport],
+                       cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["config"]["halo"] == transport
+    assert line["config"]["shared_gpu_test_mode"] is True and line["value"] > 0
+    assert line["e2e"]["value"] > 0
