@@ -192,6 +192,10 @@ typedef struct {
     const int64_t *cbase;
     const int32_t *cnf;
     const uint8_t *crank;
+    /* traversal order (may be NULL = tile order): launch position
+     * p in [tile_begin, tile_end) updates tile order[p]; a permutation that
+     * keeps z neighbours close in time keeps lines they share in L2 */
+    const int32_t *order;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);

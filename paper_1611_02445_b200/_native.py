@@ -36,7 +36,7 @@ class StepArgs(ctypes.Structure):
                 ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
                 ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int),
                 ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int),
-                ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp)]
+                ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp), ("order", c_vp)]
 
 
 _PROTOS = {

@@ -76,7 +76,8 @@ constexpr int min_blocks_compact() {
 // offsets from the copy start and each pull is one 32-bit add chain plus one
 // IMAD.WIDE.U32 from a single base -- fewer live registers than a 64-bit
 // pointer per pull.  Otherwise 64-bit block pointers are staged.
-template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32>
+template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32,
+          bool ORDERED>
 __global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT>())
 step_kernel_compact(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
@@ -86,23 +87,24 @@ step_kernel_compact(const StepParams<T, MRT> p) {
     __shared__ __align__(16) unsigned char s_rank[TPC][NBR][64];
     const int ti = threadIdx.x >> 6;
     const int j = threadIdx.x & 63;
-    const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
-    const long long tile = tile0 + ti;
+    const long long pos0 = p.tile_begin + (long long)blockIdx.x * TPC;
+    const bool valid = pos0 + ti < p.tile_end;
+    const long long tile = valid ? tile_at<ORDERED>(p, pos0 + ti) : 0;
 
     // the node word does not depend on the staging: load it first so its
     // latency overlaps the neighbour rows
-    const uint32_t meta = tile < p.tile_end ? p.meta[tile * 64 + j] : 0u;
+    const uint32_t meta = valid ? p.meta[tile * 64 + j] : 0u;
     // neighbour rows, then each neighbour's 64 ranks as four 16-byte copies
     for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
-        const long long t = tile0 + i / NBR;
+        const bool ok = pos0 + i / NBR < p.tile_end;
+        const long long t = ok ? tile_at<ORDERED>(p, pos0 + i / NBR) : 0;
         const int k = i % NBR;
         // no D3Q19 pull reads one of the 8 corner neighbours: not staged
         if (k == 0 || k == 2 || k == 6 || k == 8 || k == 18 || k == 20 || k == 24 || k == 26)
             continue;
         long long nb = -1;
-        if (t < p.tile_end)
-            nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1) : p.nbr[t * NBR + k];
-        const long long tt = nb >= 0 ? nb : (t < p.tile_end ? t : p.tile_begin);
+        if (ok) nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1) : p.nbr[t * NBR + k];
+        const long long tt = nb >= 0 ? nb : t;
         if (OFF32) s_off[OFF32 ? i / NBR : 0][k] = (unsigned)p.cbase[tt];
         else s_src[OFF32 ? 0 : i / NBR][k] = p.src + p.cbase[tt];
         s_nf[i / NBR][k] = p.cnf[tt];

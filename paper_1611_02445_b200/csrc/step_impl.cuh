@@ -56,7 +56,18 @@ struct StepParams {
     const long long *__restrict__ cbase;
     const int *__restrict__ cnf;
     const unsigned char *__restrict__ crank;
+    // traversal order (may be null = tile order): CTA position -> tile
+    const int *__restrict__ order;
 };
+
+// the tile at launch position pos (tile_begin <= pos < tile_end); ORDERED
+// kernels read the traversal order, the others keep the tile-list order
+// (a template switch: the extra pointer alone made the fp32 kernel spill)
+template <bool ORDERED, class P>
+__device__ __forceinline__ long long tile_at(const P &p, long long pos) {
+    if constexpr (ORDERED) return (long long)__ldg(p.order + pos);
+    else return pos;
+}
 
 __host__ __device__ constexpr int up_dir(int k) {
     return k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 13 : k == 3 ? 15 : 17;
@@ -196,15 +207,16 @@ __device__ const PullTable kPullTables[3] = {make_pull_table<0>(), make_pull_tab
 // (e.g. a periodic wrap across more than 1.77 M tiles) the 64-bit path stages
 // the 27 neighbour block addresses themselves and selects a pointer per pull.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32, bool MRT, bool HALO,
-          bool FMA>
+          bool FMA, bool ORDERED>
 __global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, VARIANT>())
 step_kernel(const StepParams<T, MRT> p) {
     __shared__ int s_nbr[TPC][NBR];
     __shared__ const T *s_ptr[REL32 ? 1 : TPC][NBR];
     const int ti = threadIdx.x >> 6;
     const int j = threadIdx.x & 63;
-    const long long tile0 = p.tile_begin + (long long)blockIdx.x * TPC;
-    const long long tile = tile0 + ti;
+    const long long pos0 = p.tile_begin + (long long)blockIdx.x * TPC;
+    const bool valid = pos0 + ti < p.tile_end;
+    const long long tile = valid ? tile_at<ORDERED>(p, pos0 + ti) : 0;
 
     // REL32 pulls read their packed word through the read-only path (the
     // 4.9 KB table stays L1-resident).  Measured on B200 (scripts/step_sweep.py):
@@ -221,8 +233,9 @@ step_kernel(const StepParams<T, MRT> p) {
     constexpr bool kTable = VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE >= 1;
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
-            const long long t = tile0 + i / NBR;
-            const long long nb = t < p.tile_end ? p.nbr[t * NBR + i % NBR] : -1;
+            const bool ok = pos0 + i / NBR < p.tile_end;
+            const long long t = ok ? tile_at<ORDERED>(p, pos0 + i / NBR) : 0;
+            const long long nb = ok ? p.nbr[t * NBR + i % NBR] : -1;
             const long long d = nb >= 0 ? nb - t : 0;
             s_nbr[i / NBR][i % NBR] = (int)(REL32 ? d * TILE_VALUES : d);
             if (!REL32) s_ptr[REL32 ? 0 : i / NBR][i % NBR] = p.src + (t + d) * TILE_VALUES;
@@ -230,7 +243,7 @@ step_kernel(const StepParams<T, MRT> p) {
         __syncthreads();
     }
 
-    const uint32_t meta = tile < p.tile_end ? p.meta[tile * 64 + j] : 0u;
+    const uint32_t meta = valid ? p.meta[tile * 64 + j] : 0u;
     uint32_t status = 0;
     if (meta & META_ACTIVE) {
         const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
@@ -385,7 +398,16 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int TPC = tiles_per_cta<T>();
-    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA>
+    // the traversal order is a permutation of a whole-store launch; the
+    // bench-ladder variants and the halo launches run in tile order
+    if constexpr (VARIANT == TLBM_FULL && !HALO) {
+        if (a->order) {
+            step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA, true>
+                <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+            return launch_check("step_kernel");
+        }
+    }
+    step_kernel<T, QUASI, TABLE, VARIANT, TPC, REL32, MRT, HALO, FMA, false>
         <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel");
 }
@@ -397,12 +419,24 @@ int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int TPC = compact_tiles_per_cta<T>();
+    const unsigned grid = (unsigned)((n + TPC - 1) / TPC);
+    if constexpr (VARIANT == TLBM_FULL) {
+        if (a->order) {
+            if (a->rel32)
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, true>
+                    <<<grid, 64 * TPC, 0, s>>>(p);
+            else
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, true>
+                    <<<grid, 64 * TPC, 0, s>>>(p);
+            return launch_check("step_kernel_compact");
+        }
+    }
     if (a->rel32)       // for compact storage: 19 * n_fn < 2^32 (solver.py)
-        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true>
-            <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, false>
+            <<<grid, 64 * TPC, 0, s>>>(p);
     else
-        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false>
-            <<<(unsigned)((n + TPC - 1) / TPC), 64 * TPC, 0, s>>>(p);
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, false>
+            <<<grid, 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel_compact");
 }
 
@@ -449,6 +483,7 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     p.cbase = reinterpret_cast<const long long *>(a->cbase);
     p.cnf = a->cnf;
     p.crank = a->crank;
+    p.order = a->order;
 }
 
 template <class T>

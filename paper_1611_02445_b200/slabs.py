@@ -137,7 +137,10 @@ class SlabSolver:
             raise ValueError("slab decomposition needs the block storage (storage='blocks'): "
                              "halo pack/unpack and the fused peer stores address 64-slot "
                              "blocks")
-        self.solver = Solver(self.local_geometry, config or SimulationConfig(), device)
+        # slab launches name tile ranges (boundary layers, interior), so the
+        # solver keeps the tile-list order
+        self.solver = Solver(self.local_geometry, config or SimulationConfig(), device,
+                             traversal="tile")
         s = self.solver
         layers = layer_tile_ranges(s.tiling.tile_map)
         has_lo, has_hi = self.range.lower >= 0, self.range.upper >= 0

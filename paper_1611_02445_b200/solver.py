@@ -128,10 +128,22 @@ class SimulationState:
 class Solver:
     """Device-resident tiled LBGK solver for one geometry on one GPU."""
 
-    def __init__(self, geometry, config=None, device=None, tiling=None, index64=False):
+    def __init__(self, geometry, config=None, device=None, tiling=None, index64=False,
+                 traversal="auto"):
         """``index64`` forces the step's 64-bit addressing path (used
         automatically when neighbour offsets exceed 32 bits, i.e. beyond
-        ~1.76 M tiles); exposed for tests and measurements."""
+        ~1.76 M tiles); exposed for tests and measurements.
+
+        ``traversal``: the order the step visits tiles in.  "tile" is the
+        tile-list order (z outer).  "auto" switches fp32 block storage to a
+        y-blocked order (traversal_order) when a z-layer of tiles moves more
+        bytes than L2_REUSE_BUDGET, so that the 128-byte L2 lines a tile
+        shares with its z neighbour are still resident when the neighbour
+        runs (fp32 512^3: 0.89 -> 0.93 of peak; 1024 x 1024 x 128: 0.83 ->
+        0.92).  fp64 blocks share no lines across z and lose DRAM streaming
+        locality in the blocked order (0.99 -> 0.94), so they keep the tile
+        order, as does compact storage (measured slower).  An int forces the
+        blocking with that many tile rows."""
         self.config = config if config is not None else SimulationConfig()
         self.geometry = geometry
         self.tiling = tiling if tiling is not None else DeviceTiling(geometry, device)
@@ -181,6 +193,8 @@ class Solver:
         else:
             a.collision = nat.LBGK
         self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
+        self.order = traversal_order(self.tiling, self.store, traversal)
+        a.order = self.order.data_ptr() if self.order is not None else None
         self._graphs = {}
         self._iter_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._iter_dev_value = 0
@@ -513,6 +527,46 @@ def run(config, geometry, iterations, outputs=None, device=None, check_every=STA
     if callable(outputs):
         outputs(solver)
     return solver.state, diagnostics
+
+
+L2_REUSE_BUDGET = 40 << 20    # bytes of step traffic between a tile and its z neighbour
+
+
+def traversal_order(tiling, store, traversal="auto"):
+    """Tile visiting order of the step (tlbm_step_args.order), or None for
+    the tile-list order.
+
+    The tile list is z outer, so a tile's z neighbour comes a whole layer of
+    tiles later.  Lines the two share (a 128-byte L2 line holds two fp32
+    z-planes of a block; compact blocks are not line aligned) are fetched
+    twice once a layer's traffic exceeds what L2 keeps.  The blocked order
+    visits the tiles in bands of ``yb`` tile rows, z inside a band: a z
+    neighbour is then ``yb`` rows away and a y neighbour one row, except
+    across band edges."""
+    if traversal == "tile" or tiling.t_n == 0:
+        return None
+    if traversal == "auto" and (store.flat.element_size() != 4
+                                or isinstance(store, CompactFieldStore)):
+        return None
+    ntx, nty, ntz = tiling.mesh
+    n_d = store.flat.element_size()
+    per_tile = 2.0 * store.flat.numel() / 2 / max(tiling.t_n, 1) * n_d   # read + write
+    coords = tiling.non_empty.to(torch.int64) // 4
+    if isinstance(traversal, int):
+        yb = max(1, int(traversal))
+    else:
+        layers = int(torch.unique(coords[:, 2]).numel())
+        rows = int(torch.unique(coords[:, 1] * ntz + coords[:, 2]).numel())
+        layer_bytes = tiling.t_n / max(layers, 1) * per_tile
+        if layer_bytes <= L2_REUSE_BUDGET:
+            return None
+        row_bytes = tiling.t_n / max(rows, 1) * per_tile
+        yb = max(1, int(L2_REUSE_BUDGET // max(row_bytes, 1.0)))
+        if yb >= nty:
+            return None
+    tx, ty, tz = coords[:, 0], coords[:, 1], coords[:, 2]
+    key = (((ty // yb) * ntz + tz) * nty + ty) * ntx + tx
+    return torch.argsort(key, stable=True).to(torch.int32)
 
 
 # storage="auto": compact below this tile utilisation (fp64).  From the

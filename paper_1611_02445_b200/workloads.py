@@ -61,10 +61,10 @@ def perturbed_fields(t_n, dtype, device, u0=(0.04, 0.0, 0.0), amp=1e-3, seed=123
 
 def make_solver(geo, precision="f64", fluid="incompressible", table=None, perturb=True,
                 device=None, u0=(0.04, 0.0, 0.0), index64=False, arithmetic="reference",
-                storage="blocks"):
+                storage="blocks", traversal="auto"):
     cfg = SimulationConfig(fluid=fluid, tau=TAU, precision=precision, table=table,
                            arithmetic=arithmetic, storage=storage)
-    s = Solver(geo, cfg, device=device, index64=index64)
+    s = Solver(geo, cfg, device=device, index64=index64, traversal=traversal)
     if perturb:
         rho, u = perturbed_fields(s.t_n, s.store.tdtype, s.device, u0)
         s.init_from_macroscopic(rho, u)

@@ -29,6 +29,7 @@ p.add_argument("--index64", action="store_true", help="force 64-bit addressing")
 p.add_argument("--arith", default="reference", choices=["reference", "fma"])
 p.add_argument("--graph", action="store_true", help="replay captured CUDA graphs of steps")
 p.add_argument("--storage", default="blocks", choices=["blocks", "compact"])
+p.add_argument("--traversal", default="auto", help="auto | tile | <rows per band>")
 p.add_argument("--l2-fetch", type=int, default=-1,
                help="cudaLimitMaxL2FetchGranularity in bytes (0..128; -1 leaves the default)")
 a = p.parse_args()
@@ -47,7 +48,8 @@ else:
     geo = workloads.sphere_pack(a.porosity, n=a.n)
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
                           index64=a.index64, arithmetic=a.arith, perturb=not a.no_perturb,
-                          storage=a.storage)
+                          storage=a.storage,
+                          traversal=int(a.traversal) if a.traversal.isdigit() else a.traversal)
 if a.no_perturb:
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04) if a.geometry == "channel_z" else (0.04, 0.0, 0.0))
 from paper_1611_02445_b200.solver import GRAPH_STEPS as solver_graph_steps  # noqa: E402
@@ -66,7 +68,8 @@ for v in a.variants.split(","):
         from paper_1611_02445_b200.solver import SimulationConfig, Solver
         cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision=a.precision,
                                table=a.table, u_max_guard=0.0, arithmetic=a.arith,
-                               storage=a.storage)
+                               storage=a.storage,
+                          traversal=int(a.traversal) if a.traversal.isdigit() else a.traversal)
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
         s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
@@ -82,7 +85,7 @@ for v in a.variants.split(","):
     gbs = s.n_fn * 2 * 19 * n_d / (ms / 1e3) / 1e9
     print(json.dumps({"lib": os.path.basename(nat.LIB_PATH), "index64": a.index64,
                       "arith": a.arith, "graph": a.graph, "l2_fetch": l2_fetch,
-                      "storage": a.storage,
+                      "storage": a.storage, "ordered": s.order is not None,
                       "geometry": a.geometry, "n": a.n, "dims": list(geo.shape),
                       "field_gb": round(s.store.flat.numel() * n_d / 1e9, 2),
                       "precision": a.precision, "table": a.table, "variant": v,
