@@ -216,25 +216,24 @@ step_kernel(const StepParams<T, MRT> p) {
     const int j = threadIdx.x & 63;
     const long long pos0 = p.tile_begin + (long long)blockIdx.x * TPC;
     const bool valid = pos0 + ti < p.tile_end;
-    const long long tile = valid ? tile_at<ORDERED>(p, pos0 + ti) : 0;
+    const long long tile = ORDERED ? (valid ? tile_at<ORDERED>(p, pos0 + ti) : 0) : pos0 + ti;
 
-    // REL32 pulls read their packed word through the read-only path (the
-    // 4.9 KB table stays L1-resident).  Measured on B200 (scripts/step_sweep.py):
-    // fp32 0.50 ms vs 0.51-0.56 with per-direction address arithmetic and
-    // 0.57 with a per-CTA shared-memory copy (whose 640 MB/step of staging
-    // loads cost more than they save) and 0.55 with 16-byte unpacked entries
-    // (LDG.128: the hoisted 76 registers spill); fp64 unchanged at 0.78 ms.
-#ifndef TLBM_PULL_MODE
-#define TLBM_PULL_MODE 1   // 0: computed addresses, 1: packed pull table
-#endif
+    // Pulls read their packed word through the read-only path (the 4.9 KB
+    // table stays L1-resident).  Measured on B200 (scripts/step_sweep.py, at
+    // the 32-warp fp32 shape): 0.50 ms vs 0.51-0.56 with per-direction
+    // address arithmetic, 0.57 with a per-CTA shared-memory copy (whose 640
+    // MB/step of staging loads cost more than they save) and 0.55 with
+    // 16-byte unpacked entries (LDG.128: the hoisted 76 registers spill);
+    // fp64 unchanged at 0.78 ms.
+    //
     // The neighbour row is staged as the tile-index difference to the
     // thread's own tile (0 for the own-tile entry 13); REL32 stores it
     // pre-multiplied by the 1216 values of a tile.
-    constexpr bool kTable = VARIANT != TLBM_READ_WRITE_ONLY && TLBM_PULL_MODE >= 1;
     if (VARIANT != TLBM_READ_WRITE_ONLY) {
         for (int i = threadIdx.x; i < TPC * NBR; i += 64 * TPC) {
             const bool ok = pos0 + i / NBR < p.tile_end;
-            const long long t = ok ? tile_at<ORDERED>(p, pos0 + i / NBR) : 0;
+            const long long t = ORDERED ? (ok ? tile_at<ORDERED>(p, pos0 + i / NBR) : 0)
+                                        : pos0 + i / NBR;
             const long long nb = ok ? p.nbr[t * NBR + i % NBR] : -1;
             const long long d = nb >= 0 ? nb - t : 0;
             s_nbr[i / NBR][i % NBR] = (int)(REL32 ? d * TILE_VALUES : d);
@@ -252,39 +251,22 @@ step_kernel(const StepParams<T, MRT> p) {
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            if (VARIANT == TLBM_READ_WRITE_ONLY || (!kTable && q == 0)) {
+            if (VARIANT == TLBM_READ_WRITE_ONLY) {
                 g[q] = load_ro(base + (q * 64 + slot_of<TABLE>(q, x, y, z)));
                 continue;
             }
-            if (kTable) {
-                // q = 0 needs no test: its word is (own slot, delta 13), and
-                // bit 0 of meta (the active bit) is set
-                const uint32_t w = __ldg(&kPullTables[TABLE].w[q * 64 + j]);
-                const int in_tile = (int)(w & 0x7ffu);
-                const int bounced = (int)((w >> 11) & 0x7ffu);
-                const bool link = (meta >> q) & 1u;
-                if (REL32) {
-                    const int pulled = s_nbr[ti][w >> 22] + in_tile;
-                    g[q] = load_ro(base + (link ? pulled : bounced));
-                } else {
-                    const T *src = link ? s_ptr[REL32 ? 0 : ti][w >> 22] : base;
-                    g[q] = load_ro(src + (link ? in_tile : bounced));
-                }
-                continue;
-            }
-            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
-            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
-            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
-            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
-            const int in_tile = q * 64 + slot_of<TABLE>(q, sx & 3, sy & 3, sz & 3);
-            const int bounced = opp(q) * 64 + slot_of<TABLE>(opp(q), x, y, z);
+            // q = 0 needs no test: its word is (own slot, delta 13), and bit
+            // 0 of meta (the active bit) is set
+            const uint32_t w = __ldg(&kPullTables[TABLE].w[q * 64 + j]);
+            const int in_tile = (int)(w & 0x7ffu);
+            const int bounced = (int)((w >> 11) & 0x7ffu);
             const bool link = (meta >> q) & 1u;
-            const int d = (dx | dy | dz) ? s_nbr[ti][delta_index(dx, dy, dz)] : 0;
             if (REL32) {
-                g[q] = load_ro(base + (link ? d + in_tile : bounced));
+                const int pulled = s_nbr[ti][w >> 22] + in_tile;
+                g[q] = load_ro(base + (link ? pulled : bounced));
             } else {
-                const long long rel = link ? (long long)d * TILE_VALUES : 0;
-                g[q] = load_ro(base + rel + (link ? in_tile : bounced));
+                const T *src = link ? s_ptr[REL32 ? 0 : ti][w >> 22] : base;
+                g[q] = load_ro(src + (link ? in_tile : bounced));
             }
         }
 
