@@ -10,14 +10,15 @@ point ``tilelbm.cli:main`` has no module behind it).
 
 Geometry mini-language: cavity:N, channel:square|circle:d:off1:off2:len[:ends],
 spheres:n:diam:porosity:seed, box:n, vessel:nx:ny:nz, file:path (TLBM1).
-Exit codes: 0 ok, 2 usage, 3 divergence, 4 I/O.
+Exit codes: 0 ok, 2 usage, 3 divergence, 4 I/O, 5 runtime (no CUDA device,
+library error, invalid configuration).
 """
 
 import argparse
 import json
 import sys
 
-EXIT_OK, EXIT_USAGE, EXIT_DIVERGED, EXIT_IO = 0, 2, 3, 4
+EXIT_OK, EXIT_USAGE, EXIT_DIVERGED, EXIT_IO, EXIT_RUNTIME = 0, 2, 3, 4, 5
 
 
 class UsageError(ValueError):
@@ -214,6 +215,9 @@ def main(argv=None):
     except OSError as exc:
         print(f"I/O error: {exc}", file=sys.stderr)
         return EXIT_IO
+    except (RuntimeError, ValueError) as exc:   # no CUDA device, library errors, bad config
+        print(f"error: {exc}", file=sys.stderr)
+        return EXIT_RUNTIME
 
 
 if __name__ == "__main__":

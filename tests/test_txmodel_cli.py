@@ -95,3 +95,10 @@ def test_perf_model_matches_reference(reference):
     for kw in ({}, {"n_d": 4}, {"q": 27, "n_d": 8, "n_t": 2}):
         ours, ref = txmodel.PerfModel(**kw), reference.txmodel.PerfModel(**kw)
         assert (ours.m_node(), ours.b_node()) == (ref.m_node(), ref.b_node())
+
+
+def test_cli_runtime_error_exit_code(capsys):
+    """A solver command without a usable configuration fails with exit code 5
+    and a one-line message (no traceback)."""
+    assert cli.main(["run", "--geometry", "cavity:8", "--precision", "f32", "--arith", "fma"]) == 5
+    assert "f64-only" in capsys.readouterr().err
