@@ -92,11 +92,11 @@ using namespace tlbm;
 
 extern "C" int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank,
                                   void *stream) {
+    if (t_n == 0) return TLBM_OK;             // no tiles: nothing to rank
     if (!d_meta || !d_rank || t_n < 0) {
         set_error("tlbm_compact_ranks: bad argument");
         return TLBM_ERR_ARG;
     }
-    if (t_n == 0) return TLBM_OK;
     ranks_kernel<<<(unsigned)((t_n * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
         d_meta, (long long)t_n, d_rank);
     return launch_check("ranks_kernel");
@@ -112,11 +112,11 @@ extern "C" int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, in
                   table);
         return TLBM_ERR_ARG;
     }
+    if (t_n == 0) return TLBM_OK;
     if (!d_in || !d_out || !d_base || !d_nf || !d_rank) {
         set_error("tlbm_compact_convert: null argument");
         return TLBM_ERR_ARG;
     }
-    if (t_n == 0) return TLBM_OK;
     cudaStream_t s = as_stream(stream);
     return dtype == TLBM_F64 ? convert_as<double>(d_in, d_out, t_n, d_base, d_nf, d_rank,
                                                   to_compact, s)

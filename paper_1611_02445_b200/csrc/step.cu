@@ -26,7 +26,13 @@ int step_launch_f32(const tlbm_step_args *a, cudaStream_t s);
 using namespace tlbm;
 
 extern "C" int tlbm_step(const tlbm_step_args *a, void *stream) {
-    if (!a || !a->f_src || !a->f_dst || !a->meta ||
+    if (!a) {
+        set_error("tlbm_step: null argument");
+        return TLBM_ERR_ARG;
+    }
+    // an empty store (all-solid geometry) has no buffers and nothing to do
+    if (a->t_n == 0 && a->tile_begin == 0 && a->tile_end == 0) return TLBM_OK;
+    if (!a->f_src || !a->f_dst || !a->meta ||
         (a->variant != TLBM_READ_WRITE_ONLY && !a->nbr)) {
         set_error("tlbm_step: null argument");
         return TLBM_ERR_ARG;
