@@ -33,6 +33,7 @@ p.add_argument("--traversal", default="auto", help="auto | tile | <rows per band
 p.add_argument("--l2-fetch", type=int, default=-1,
                help="cudaLimitMaxL2FetchGranularity in bytes (0..128; -1 leaves the default)")
 a = p.parse_args()
+traversal = int(a.traversal) if a.traversal.isdigit() else a.traversal
 if a.geometry == "channel":
     geo = workloads.channel(a.n)
 elif a.geometry == "channel_z":
@@ -49,7 +50,7 @@ else:
 s = workloads.make_solver(geo, precision=a.precision, table=a.table, u0=(0.04, 0, 0),
                           index64=a.index64, arithmetic=a.arith, perturb=not a.no_perturb,
                           storage=a.storage,
-                          traversal=int(a.traversal) if a.traversal.isdigit() else a.traversal)
+                          traversal=traversal)
 if a.no_perturb:
     s.init_equilibrium(1.0, (0.0, 0.0, 0.04) if a.geometry == "channel_z" else (0.04, 0.0, 0.0))
 from paper_1611_02445_b200.solver import GRAPH_STEPS as solver_graph_steps  # noqa: E402
@@ -68,11 +69,10 @@ for v in a.variants.split(","):
         from paper_1611_02445_b200.solver import SimulationConfig, Solver
         cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision=a.precision,
                                table=a.table, u_max_guard=0.0, arithmetic=a.arith,
-                               storage=a.storage,
-                          traversal=int(a.traversal) if a.traversal.isdigit() else a.traversal)
+                               storage=a.storage)
         del solvers["lbgk"], s
         torch.cuda.empty_cache()
-        s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64)
+        s = solvers["mrt"] = Solver(geo, cfg, index64=a.index64, traversal=traversal)
     s.step(solver_graph_steps if a.graph else 5, variant=vmap[v], check=False, graph=a.graph)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
