@@ -196,6 +196,11 @@ typedef struct {
      * p in [tile_begin, tile_end) updates tile order[p]; a permutation that
      * keeps z neighbours close in time keeps lines they share in L2 */
     const int32_t *order;
+    /* fused halo on compact storage: the neighbour's block offsets (cbase)
+     * of its ghost tiles, indexed tile - halo_*_begin; halo_up / halo_down
+     * then point at the neighbour's copy, not at its ghost layer */
+    const int64_t *halo_up_cbase;
+    const int64_t *halo_down_cbase;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);
@@ -209,6 +214,11 @@ int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank, voi
 int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, int table,
                          int64_t t_n, const int64_t *d_base, const int32_t *d_nf,
                          const uint8_t *d_rank, int to_compact, void *stream);
+
+/* tlbm_halo on a compact store (same packed buffer; solid slots pack as 0). */
+int tlbm_halo_compact(void *d_f, int dtype, int64_t tile_begin, int64_t tile_end, int up,
+                      int pack, void *d_buf, const int64_t *d_base, const int32_t *d_nf,
+                      const uint8_t *d_rank, void *stream);
 
 /* *d_counter += k (one thread; the last node of a captured step graph). */
 int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream);

@@ -36,7 +36,8 @@ class StepArgs(ctypes.Structure):
                 ("halo_down", c_vp), ("halo_down_begin", c_i64), ("halo_down_end", c_i64),
                 ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int),
                 ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int),
-                ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp), ("order", c_vp)]
+                ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp), ("order", c_vp),
+                ("halo_up_cbase", c_vp), ("halo_down_cbase", c_vp)]
 
 
 _PROTOS = {
@@ -74,6 +75,8 @@ _PROTOS = {
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
     "tlbm_advance_counter": (c_int, [c_vp, c_i64, c_vp]),
     "tlbm_compact_ranks": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "tlbm_halo_compact": (c_int, [c_vp, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
+                                  c_vp, c_vp]),
     "tlbm_compact_convert": (c_int, [c_vp, c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp, c_int,
                                      c_vp]),
     "tlbm_ipc_export": (c_int, [c_vp, c_vp, ctypes.POINTER(ctypes.c_uint64)]),

@@ -123,3 +123,81 @@ extern "C" int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, in
                              : convert_as<float>(d_in, d_out, t_n, d_base, d_nf, d_rank,
                                                  to_compact, s);
 }
+
+// ---- slab halo on a compact store (fields.cu: halo_kernel for blocks) -----
+// Same packed buffer as tlbm_halo -- buf[(tile - tile_begin) * 80 + k * 16 +
+// (x + 4 y)] for the 5 directions crossing the outer z plane -- with each
+// value found at base + q * nf + rank; solid slots pack as 0 and are skipped
+// on unpack.
+namespace tlbm {
+namespace {
+
+__host__ __device__ constexpr int compact_halo_dir(int up, int k) {
+    return up ? (k == 0 ? 5 : k == 1 ? 11 : k == 2 ? 13 : k == 3 ? 15 : 17)
+              : (k == 0 ? 6 : k == 1 ? 12 : k == 2 ? 14 : k == 3 ? 16 : 18);
+}
+
+template <class T, bool UP, bool PACK>
+__global__ void halo_compact_kernel(T *f, long long tile_begin, long long n_tiles, T *buf,
+                                    const long long *base, const int *nf,
+                                    const unsigned char *rank) {
+    const long long n = n_tiles * 80;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long t = tile_begin + i / 80;
+        const int r = (int)(i % 80);
+        const int k = r >> 4, s = r & 15;
+        const int j = s + 16 * (UP ? 3 : 0);
+        const int rk = rank[t * 64 + j];
+        int q = 0;
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk)
+            if (kk == k) q = compact_halo_dir(UP, kk);
+        if (rk == 255) {
+            if (PACK) buf[i] = T(0);
+            continue;
+        }
+        const long long at = base[t] + (long long)q * nf[t] + rk;
+        if (PACK) buf[i] = f[at];
+        else f[at] = buf[i];
+    }
+}
+
+template <class T>
+int halo_compact_as(void *d_f, int64_t tile_begin, int64_t nt, int up, int pack, void *d_buf,
+                    const int64_t *d_base, const int32_t *d_nf, const uint8_t *d_rank,
+                    cudaStream_t s) {
+    auto *f = static_cast<T *>(d_f);
+    auto *b = static_cast<T *>(d_buf);
+    const auto *base = reinterpret_cast<const long long *>(d_base);
+    const unsigned g = grid_for_slots(nt * 80);
+    if (up && pack) halo_compact_kernel<T, true, true><<<g, 256, 0, s>>>(f, tile_begin, nt, b, base, d_nf, d_rank);
+    else if (up) halo_compact_kernel<T, true, false><<<g, 256, 0, s>>>(f, tile_begin, nt, b, base, d_nf, d_rank);
+    else if (pack) halo_compact_kernel<T, false, true><<<g, 256, 0, s>>>(f, tile_begin, nt, b, base, d_nf, d_rank);
+    else halo_compact_kernel<T, false, false><<<g, 256, 0, s>>>(f, tile_begin, nt, b, base, d_nf, d_rank);
+    return launch_check("halo_compact_kernel");
+}
+
+}  // namespace
+}  // namespace tlbm
+
+extern "C" int tlbm_halo_compact(void *d_f, int dtype, int64_t tile_begin, int64_t tile_end,
+                                 int up, int pack, void *d_buf, const int64_t *d_base,
+                                 const int32_t *d_nf, const uint8_t *d_rank, void *stream) {
+    if (tile_end < tile_begin || tile_begin < 0) {
+        set_error("tlbm_halo_compact: bad tile range");
+        return TLBM_ERR_ARG;
+    }
+    const long long nt = tile_end - tile_begin;
+    if (nt == 0) return TLBM_OK;
+    int rc;
+    if ((rc = check_dtype(dtype))) return rc;
+    if (!d_f || !d_buf || !d_base || !d_nf || !d_rank) {
+        set_error("tlbm_halo_compact: null argument");
+        return TLBM_ERR_ARG;
+    }
+    cudaStream_t s = as_stream(stream);
+    return dtype == TLBM_F64
+               ? halo_compact_as<double>(d_f, tile_begin, nt, up, pack, d_buf, d_base, d_nf, d_rank, s)
+               : halo_compact_as<float>(d_f, tile_begin, nt, up, pack, d_buf, d_base, d_nf, d_rank, s);
+}

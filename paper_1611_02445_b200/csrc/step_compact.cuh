@@ -77,7 +77,7 @@ constexpr int min_blocks_compact() {
 // IMAD.WIDE.U32 from a single base -- fewer live registers than a 64-bit
 // pointer per pull.  Otherwise 64-bit block pointers are staged.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32,
-          bool ORDERED>
+          bool ORDERED, bool HALO>
 __global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT>())
 step_kernel_compact(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
@@ -168,6 +168,23 @@ step_kernel_compact(const StepParams<T, MRT> p) {
         T *out = p.dst + (own_src - p.src);
 #pragma unroll
         for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
+        if constexpr (HALO) {
+            // fused halo: the neighbour's ghost copy of this tile has the same
+            // nodes (same ranks and count), at its own block offset
+            const int z = j >> 4;
+            if (p.halo_up && z == 3 && tile >= p.halo_up_begin && tile < p.halo_up_end) {
+                T *peer = p.halo_up + p.halo_up_cbase[tile - p.halo_up_begin];
+#pragma unroll
+                for (int k = 0; k < 5; ++k)
+                    peer[up_dir(k) * nf_own + rank_own] = g[up_dir(k)];
+            }
+            if (p.halo_down && z == 0 && tile >= p.halo_down_begin && tile < p.halo_down_end) {
+                T *peer = p.halo_down + p.halo_down_cbase[tile - p.halo_down_begin];
+#pragma unroll
+                for (int k = 0; k < 5; ++k)
+                    peer[opp(up_dir(k)) * nf_own + rank_own] = g[opp(up_dir(k))];
+            }
+        }
     }
     if (p.flags) {
         const uint32_t any = __reduce_or_sync(0xffffffffu, status);

@@ -58,6 +58,9 @@ struct StepParams {
     const unsigned char *__restrict__ crank;
     // traversal order (may be null = tile order): CTA position -> tile
     const int *__restrict__ order;
+    // fused halo on compact storage: neighbour block offsets of its ghosts
+    const long long *halo_up_cbase;
+    const long long *halo_down_cbase;
 };
 
 // the tile at launch position pos (tile_begin <= pos < tile_end); ORDERED
@@ -403,29 +406,41 @@ int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
     constexpr int TPC = compact_tiles_per_cta<T>();
     const unsigned grid = (unsigned)((n + TPC - 1) / TPC);
     if constexpr (VARIANT == TLBM_FULL) {
-        if (a->order) {
+        if (a->halo_up || a->halo_down) {
             if (a->rel32)
-                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, true>
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, false, true>
                     <<<grid, 64 * TPC, 0, s>>>(p);
             else
-                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, true>
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, false, true>
+                    <<<grid, 64 * TPC, 0, s>>>(p);
+            return launch_check("step_kernel_compact");
+        }
+        if (a->order) {
+            if (a->rel32)
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, true, false>
+                    <<<grid, 64 * TPC, 0, s>>>(p);
+            else
+                step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, true, false>
                     <<<grid, 64 * TPC, 0, s>>>(p);
             return launch_check("step_kernel_compact");
         }
     }
     if (a->rel32)       // for compact storage: 19 * n_fn < 2^32 (solver.py)
-        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, false>
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, true, false, false>
             <<<grid, 64 * TPC, 0, s>>>(p);
     else
-        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, false>
+        step_kernel_compact<T, QUASI, TABLE, VARIANT, TPC, MRT, FMA, false, false, false>
             <<<grid, 64 * TPC, 0, s>>>(p);
     return launch_check("step_kernel_compact");
 }
 
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT>
 int launch_compact(const tlbm_step_args *a, cudaStream_t s) {
-    if (a->halo_up || a->halo_down) {
-        set_error("tlbm_step: the fused halo does not support compact storage");
+    const bool halo = a->halo_up || a->halo_down;
+    if (halo && (VARIANT != TLBM_FULL || a->order ||
+                 (a->halo_up && !a->halo_up_cbase) || (a->halo_down && !a->halo_down_cbase))) {
+        set_error("tlbm_step: the compact fused halo needs the full step in tile order and "
+                  "the neighbours' ghost block offsets (halo_*_cbase)");
         return TLBM_ERR_ARG;
     }
     if (!a->cbase || !a->cnf) {
@@ -466,6 +481,8 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     p.cnf = a->cnf;
     p.crank = a->crank;
     p.order = a->order;
+    p.halo_up_cbase = reinterpret_cast<const long long *>(a->halo_up_cbase);
+    p.halo_down_cbase = reinterpret_cast<const long long *>(a->halo_down_cbase);
 }
 
 template <class T>

@@ -123,6 +123,18 @@ def layer_tile_ranges(tile_map):
     return [(int(b), int(e)) for b, e in zip(begins, ends)]
 
 
+def resolve_auto_storage_global(config, geometry):
+    """storage="auto" decided on the whole geometry's tile utilisation, so
+    that every slab rank picks the same storage."""
+    from .solver import resolve_auto_storage
+    t = np.asarray(geometry.types) != 0
+    pad = [(0, (-n) % TILE) for n in t.shape]
+    occ = np.pad(t, pad).reshape(t.shape[0] // TILE + (1 if pad[0][1] else 0), TILE,
+                                 -1, TILE, t.shape[2] // TILE + (1 if pad[2][1] else 0), TILE)
+    t_n = int(occ.any(axis=(1, 3, 5)).sum())
+    return resolve_auto_storage(config, int(t.sum()), t_n)
+
+
 class SlabSolver:
     """One rank's slab: a local Solver plus the halo bookkeeping."""
 
@@ -131,12 +143,9 @@ class SlabSolver:
         self.range = plan.ranges[rank]
         self.local_geometry = plan.local_geometry(geometry, rank)
         if config is not None and config.storage == "auto":
-            import dataclasses
-            config = dataclasses.replace(config, storage="blocks", table=None)
-        if config is not None and config.storage != "blocks":
-            raise ValueError("slab decomposition needs the block storage (storage='blocks'): "
-                             "halo pack/unpack and the fused peer stores address 64-slot "
-                             "blocks")
+            # every rank must use the same storage (the fused halo writes into
+            # the neighbour's store): decide on the whole geometry
+            config = resolve_auto_storage_global(config, geometry)
         # slab launches name tile ranges (boundary layers, interior), so the
         # solver keeps the tile-list order
         self.solver = Solver(self.local_geometry, config or SimulationConfig(), device,
@@ -233,8 +242,24 @@ class SlabSolver:
 
     def _halo(self, rng, up, pack, buf, copy):
         s = self.solver
-        nat.call("tlbm_halo", nat.ptr(s.store.copy_tensor(copy)), s.code, s.table,
+        st = s.store
+        if s.config.storage == "compact":
+            nat.call("tlbm_halo_compact", nat.ptr(st.copy_tensor(copy)), s.code, rng[0], rng[1],
+                     int(up), int(pack), nat.ptr(buf), nat.ptr(st.base), nat.ptr(st.nf),
+                     nat.ptr(st.rank), nat.stream_ptr(s.device))
+            return
+        nat.call("tlbm_halo", nat.ptr(st.copy_tensor(copy)), s.code, s.table,
                  rng[0], rng[1], int(up), int(pack), nat.ptr(buf), nat.stream_ptr(s.device))
+
+    @property
+    def compact(self):
+        return self.solver.config.storage == "compact"
+
+    def ghost_cbase(self, which):
+        """Block offsets of the ghost layer ``which`` ("lo" | "hi") of a
+        compact store (where a neighbour's fused halo writes)."""
+        g = self.ghost_lo if which == "lo" else self.ghost_hi
+        return self.solver.store.base[g[0]:g[1]]
 
     def pack(self, current=False):
         """Pack the outgoing planes of the copy just written (or, with
@@ -338,6 +363,12 @@ class IpcHalo:
         self.timeout_ns = int(timeout_s * 1e9)
         info = {"t_n": s.t_n, "ghost_lo": slab.ghost_lo, "ghost_hi": slab.ghost_hi,
                 "top": slab.top, "bottom": slab.bottom, "esize": self.esize,
+                "copy_bytes": s.store.copy_tensor(0).numel() * self.esize,
+                "compact": slab.compact,
+                "ghost_lo_cbase": (slab.ghost_cbase("lo").cpu().tolist()
+                                   if slab.compact and slab.ghost_lo else None),
+                "ghost_hi_cbase": (slab.ghost_cbase("hi").cpu().tolist()
+                                   if slab.compact and slab.ghost_hi else None),
                 "store": _export(s.store.flat), "inbox": _export(self.inbox)}
         torch.cuda.synchronize()
         infos = [None] * slab.plan.world
@@ -364,20 +395,30 @@ class IpcHalo:
             self.bases = []
             raise RuntimeError(f"peer mapping failed on some rank ({error})")
         tv = 19 * 64 * self.esize
-        self.up = None
+        if any(i["compact"] != slab.compact for i in infos):
+            raise AssertionError("slab ranks disagree on the storage")
+        dev = s.device
+        cb = lambda v: torch.tensor(v, dtype=torch.int64, device=dev)  # noqa: E731
+        self.up = self.up_cbase = None
         if r.upper >= 0:
             u = infos[r.upper]
             if u["ghost_lo"][1] - u["ghost_lo"][0] != slab.top[1] - slab.top[0]:
                 raise AssertionError("top layer and upper ghost layer differ")
-            self.up = (mapped[r.upper][0] + u["ghost_lo"][0] * tv, u["t_n"] * tv,
-                       mapped[r.upper][1] + 0)              # -> upper's "from lower" slot
-        self.down = None
+            # (ghost tiles' base, bytes per copy, inbox slot) -- a compact
+            # store's ghost tiles are found through their block offsets
+            ghost = mapped[r.upper][0] + (0 if slab.compact else u["ghost_lo"][0] * tv)
+            self.up = (ghost, u["copy_bytes"], mapped[r.upper][1] + 0)  # upper's "from lower"
+            if slab.compact:
+                self.up_cbase = cb(u["ghost_lo_cbase"])
+        self.down = self.down_cbase = None
         if r.lower >= 0:
             lo = infos[r.lower]
             if lo["ghost_hi"][1] - lo["ghost_hi"][0] != slab.bottom[1] - slab.bottom[0]:
                 raise AssertionError("bottom layer and lower ghost layer differ")
-            self.down = (mapped[r.lower][0] + lo["ghost_hi"][0] * tv, lo["t_n"] * tv,
-                         mapped[r.lower][1] + 8)            # -> lower's "from upper" slot
+            ghost = mapped[r.lower][0] + (0 if slab.compact else lo["ghost_hi"][0] * tv)
+            self.down = (ghost, lo["copy_bytes"], mapped[r.lower][1] + 8)  # lower's "from upper"
+            if slab.compact:
+                self.down_cbase = cb(lo["ghost_hi_cbase"])
         base = self.inbox.data_ptr()
         if r.lower >= 0 and r.upper >= 0:
             self.wait_ptr, self.wait_n = base, 2
@@ -403,10 +444,13 @@ class IpcHalo:
             ghost, copy_bytes, _ = self.up
             a.halo_up = ghost + dst_copy * copy_bytes
             a.halo_up_begin, a.halo_up_end = sl.top
+            a.halo_up_cbase = self.up_cbase.data_ptr() if self.up_cbase is not None else None
         if self.down is not None:
             ghost, copy_bytes, _ = self.down
             a.halo_down = ghost + dst_copy * copy_bytes
             a.halo_down_begin, a.halo_down_end = sl.bottom
+            a.halo_down_cbase = (self.down_cbase.data_ptr() if self.down_cbase is not None
+                                 else None)
 
     def disarm(self):
         a = self.slab.solver._args
@@ -613,11 +657,19 @@ class VirtualSlabs:
         tile_bytes = 19 * 64 * sl.solver.store.flat.element_size()
         if r.upper >= 0:
             u = self.slabs[r.upper]
-            a.halo_up = u.solver.store.copy_tensor(dst).data_ptr() + u.ghost_lo[0] * tile_bytes
+            a.halo_up = u.solver.store.copy_tensor(dst).data_ptr()
+            if sl.compact:
+                a.halo_up_cbase = u.ghost_cbase("lo").data_ptr()
+            else:
+                a.halo_up += u.ghost_lo[0] * tile_bytes
             a.halo_up_begin, a.halo_up_end = sl.top
         if r.lower >= 0:
             lo = self.slabs[r.lower]
-            a.halo_down = lo.solver.store.copy_tensor(dst).data_ptr() + lo.ghost_hi[0] * tile_bytes
+            a.halo_down = lo.solver.store.copy_tensor(dst).data_ptr()
+            if sl.compact:
+                a.halo_down_cbase = lo.ghost_cbase("hi").data_ptr()
+            else:
+                a.halo_down += lo.ghost_hi[0] * tile_bytes
             a.halo_down_begin, a.halo_down_end = sl.bottom
 
     def fields_owned(self):

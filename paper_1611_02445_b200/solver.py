@@ -13,7 +13,7 @@ step semantics are restated in SURVEY Appendix A).  API:
                       stated 1e-12 tolerance; f64 only), and ``storage``:
                       "blocks" (default, the paper's 64-slot blocks) or
                       "compact" (only the non-solid slots of every block;
-                      less DRAM traffic on sparse geometries, single GPU)
+                      less DRAM traffic on sparse geometries)
                       or "auto" (compact for fp64 when the tile
                       utilisation eta_t < AUTO_COMPACT_ETA, else blocks).
 ``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,

@@ -43,9 +43,6 @@ def test_rejects_unsupported_configs():
             solver.SimulationConfig(storage="compact", table=t)
     with pytest.raises(ValueError):
         solver.SimulationConfig(storage="sparse")
-    geo = geometry.generate_channel("square", 8, axis=2, length=16, ends="periodic")
-    with pytest.raises(ValueError, match="block storage"):
-        slabs.VirtualSlabs(geo, 2, solver.SimulationConfig(storage="compact"))
 
 
 @pytest.mark.parametrize("dn", DTYPES)

@@ -100,22 +100,29 @@ def test_slab_channel_single_rank_runs():
 
 COLLISIONS = {"lbgk": {}, "mrt": {"collision": "mrt"},
               "mrt_fma": {"collision": "mrt", "arithmetic": "fma"},
-              "lbgk_fma_quasi": {"arithmetic": "fma", "fluid": "quasi-compressible"}}
+              "lbgk_fma_quasi": {"arithmetic": "fma", "fluid": "quasi-compressible"},
+              "compact": {"storage": "compact"},
+              "compact_f32_mrt": {"storage": "compact", "precision": "f32", "collision": "mrt"},
+              "auto": {"storage": "auto"}}
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("coll", [c for c in COLLISIONS if c != "lbgk"])
 @pytest.mark.parametrize("name", ["pack_io", "chan_periodic"])
-def test_virtual_slabs_collision_modes(name, coll):
-    """MRT and FMA arithmetic through the slab decomposition: bit-identical
+def test_virtual_slabs_collision_modes(name, coll, fused):
+    """MRT, FMA arithmetic and compact storage through the slab
+    decomposition (halo pack/unpack, or the fused peer stores): bit-identical
     to the single-domain step with the same configuration."""
     geo = CASES[name]()
     cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
-    f0 = _f0(geo, np.float64)
+    if cfg.storage == "auto":
+        cfg = slabs.resolve_auto_storage_global(cfg, geo)
+    f0 = _f0(geo, cfg.dtype)
     ref = solver.Solver(geo, cfg)
     ref.set_fields_canonical(dense.to_canonical(f0, ref.tile_grid.non_empty, np.zeros(19)))
     ref.step(8)
     want = ref.to_dense(ref.fields_canonical(device=True))
-    vs = slabs.VirtualSlabs(geo, 3, cfg)
+    vs = slabs.VirtualSlabs(geo, 3, cfg, fused=fused)
     for sl in vs.slabs:
         s = sl.solver
         fl = _local_f(f0, sl.range, geo.shape[2])
@@ -160,7 +167,8 @@ def _mp_worker(rank, world, port, steps, out, transport="gloo", coll="lbgk"):
 
 
 @pytest.mark.parametrize("transport,coll", [("gloo", "lbgk"), ("ipc", "lbgk"), ("ipc", "mrt"),
-                                            ("ipc", "mrt_fma")])
+                                            ("ipc", "mrt_fma"), ("ipc", "compact"),
+                                            ("gloo", "compact")])
 @pytest.mark.parametrize("world", [2, 3])
 def test_multiprocess_runner_on_one_gpu(world, transport, coll):
     """DistributedSlabRunner in `world` processes sharing cuda:0 == the
