@@ -28,8 +28,9 @@ for coll in ("lbgk", "mrt"):
     s.step(2)
 chan = geometry.generate_channel("square", 12, axis=2, length=24, ends="periodic")
 for fused in (False, True):
-    vs = slabs.VirtualSlabs(chan, 3, fused=fused)
-    vs.step(3)
+    for storage in ("blocks", "compact"):
+        vs = slabs.VirtualSlabs(chan, 3, solver.SimulationConfig(storage=storage), fused=fused)
+        vs.step(3)
 for prec in ("f64", "f32"):
     s = solver.Solver(geo, solver.SimulationConfig(precision=prec, storage="compact"))
     s.step(2)
