@@ -68,7 +68,8 @@ def cmd_run(args):
     outputs = {"vtk": args.vtk, "csv": args.csv, "checkpoint": args.checkpoint,
                "convergence_every": args.convergence_every, "tolerance": args.tolerance}
     _, diag = solver.run(_config(args), geo, args.iters, outputs=outputs,
-                         resume_from=args.resume, graph=args.graph)
+                         resume_from=args.resume,
+                         graph={"auto": "auto", "on": True, "off": False}[args.graph])
     print(json.dumps(diag))
     return EXIT_OK
 
@@ -177,7 +178,8 @@ def build_parser():
     r.add_argument("--tolerance", type=float)
     r.add_argument("--checkpoint", help="save the final state here (.npz)")
     r.add_argument("--resume", help="start from this checkpoint (same geometry)")
-    r.add_argument("--graph", action="store_true", help="replay CUDA graphs of 64 steps")
+    r.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                   help="replay CUDA graphs of 64 steps (auto: small domains)")
     b = sub.add_parser("bench")
     sim_args(b)
     b.add_argument("--variant", default="full", choices=["full", "prop", "rw"])

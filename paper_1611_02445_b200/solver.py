@@ -47,6 +47,7 @@ from .tiling import DeviceTiling
 
 STATUS_RING = 4096
 GRAPH_STEPS = 64      # steps per captured CUDA graph (even: the parity is restored)
+GRAPH_AUTO_TILES = 65536    # run(graph="auto"): replay graphs up to this many tiles
 
 
 class CompressibilityWarning(UserWarning):
@@ -355,7 +356,13 @@ class Solver:
                           f"{self.guard_iterations[-1]}", CompressibilityWarning, stacklevel=2)
         self._checked = self.iteration
 
-    def run(self, iterations, check_every=STATUS_RING, graph=False):
+    def run(self, iterations, check_every=STATUS_RING, graph="auto"):
+        """``iterations`` steps, the status ring checked every ``check_every``.
+        ``graph="auto"`` replays CUDA graphs when a step is short enough for
+        the per-launch cost to show (t_n <= GRAPH_AUTO_TILES; cavity 64^3:
+        16.4 -> 13.3 us per step); True / False force it."""
+        if graph == "auto":
+            graph = 0 < self.t_n <= GRAPH_AUTO_TILES
         left = int(iterations)
         while left > 0:
             k = min(left, check_every)
@@ -479,7 +486,7 @@ def step(state):
 
 
 def run(config, geometry, iterations, outputs=None, device=None, check_every=STATUS_RING,
-        resume_from=None, graph=False):
+        resume_from=None, graph="auto"):
     """Iterate ``iterations`` steps (SPEC.md:403-410); returns (state,
     diagnostics).
 

@@ -47,7 +47,7 @@ def test_resume_rejects_other_geometry(tmp_path):
 
 def test_cli_run_checkpoint_resume(tmp_path, capsys):
     ck1, ck2 = tmp_path / "a.npz", tmp_path / "b.npz"
-    assert cli.main(["run", "--geometry", "cavity:16", "--iters", "70", "--graph",
+    assert cli.main(["run", "--geometry", "cavity:16", "--iters", "70", "--graph", "on",
                      "--checkpoint", str(ck1)]) == 0
     assert cli.main(["run", "--geometry", "cavity:16", "--iters", "30", "--resume", str(ck1),
                      "--checkpoint", str(ck2)]) == 0
