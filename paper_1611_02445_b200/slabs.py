@@ -128,10 +128,10 @@ def resolve_auto_storage_global(config, geometry):
     that every slab rank picks the same storage."""
     from .solver import resolve_auto_storage
     t = np.asarray(geometry.types) != 0
-    pad = [(0, (-n) % TILE) for n in t.shape]
-    occ = np.pad(t, pad).reshape(t.shape[0] // TILE + (1 if pad[0][1] else 0), TILE,
-                                 -1, TILE, t.shape[2] // TILE + (1 if pad[2][1] else 0), TILE)
-    t_n = int(occ.any(axis=(1, 3, 5)).sum())
+    mesh = tuple(-(-n // TILE) for n in t.shape)
+    occ = np.zeros(tuple(m * TILE for m in mesh), dtype=bool)
+    occ[:t.shape[0], :t.shape[1], :t.shape[2]] = t
+    t_n = int(occ.reshape(mesh[0], TILE, mesh[1], TILE, mesh[2], TILE).any(axis=(1, 3, 5)).sum())
     return resolve_auto_storage(config, int(t.sum()), t_n)
 
 
