@@ -125,6 +125,15 @@ def cmd_tile_stats(args):
     return EXIT_OK
 
 
+def cmd_plan(args):
+    """Size an N-GPU slab run on the host (no GPU needed)."""
+    from . import slabs
+    geo = parse_geometry(args.geometry)
+    print(json.dumps(slabs.plan_run(geo, args.gpus, args.precision, args.storage,
+                                    args.budget_gb)))
+    return EXIT_OK
+
+
 def cmd_count_tx(args):
     from . import layout, txmodel
     table = layout.LayoutTable(args.layout)
@@ -192,12 +201,18 @@ def build_parser():
     c = sub.add_parser("count-tx")
     c.add_argument("--precision", default="f64", choices=["f64", "f32"])
     c.add_argument("--layout", default="optimized", choices=["b200", "optimized", "xyz"])
+    pl = sub.add_parser("plan", help="per-rank tiles, memory and halo bytes of an N-GPU run")
+    pl.add_argument("--geometry", default="cavity:48")
+    pl.add_argument("--gpus", type=int, default=1)
+    pl.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    pl.add_argument("--storage", default="blocks", choices=["blocks", "compact", "auto"])
+    pl.add_argument("--budget-gb", type=float, default=179.0)
     sub.add_parser("info")
     return p
 
 
 COMMANDS = {"run": cmd_run, "bench": cmd_bench, "tile-stats": cmd_tile_stats,
-            "count-tx": cmd_count_tx, "info": cmd_info}
+            "count-tx": cmd_count_tx, "plan": cmd_plan, "info": cmd_info}
 
 
 def main(argv=None):

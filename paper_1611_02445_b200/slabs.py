@@ -692,3 +692,39 @@ class SlabChannel(DistributedSlabRunner):
                                             seed=1234 + rank)
         s.init_from_macroscopic(rho, u)
         self.exchange_current()
+
+
+def plan_run(geometry, world, precision="f64", storage="blocks", budget_gb=179.0):
+    """Host-only sizing of an N-GPU run (no device needed): per rank the z
+    range, tiles (owned + ghost), non-solid nodes, bytes of fields and
+    metadata, halo bytes per step, and whether it fits ``budget_gb``.
+    Field bytes: 2 copies x 19 values per slot (blocks) or per non-solid
+    node (compact); metadata 364 B per tile (node words + neighbour row),
+    plus 76 B per tile for compact storage."""
+    from .solver import SimulationConfig
+    cfg = SimulationConfig(precision=precision, storage=storage)
+    if cfg.storage == "auto":
+        cfg = resolve_auto_storage_global(cfg, geometry)
+    n_d = 8 if precision == "f64" else 4
+    plan = SlabPlan(geometry, world)
+    ranks = []
+    for r in range(world):
+        t = np.asarray(plan.local_types(geometry.types, r) if world > 1 else geometry.types) != 0
+        mesh = tuple(-(-n // TILE) for n in t.shape)
+        occ = np.zeros(tuple(m * TILE for m in mesh), dtype=bool)
+        occ[:t.shape[0], :t.shape[1], :t.shape[2]] = t
+        per_tile = occ.reshape(mesh[0], TILE, mesh[1], TILE, mesh[2], TILE).sum(axis=(1, 3, 5))
+        t_n, n_fn = int((per_tile > 0).sum()), int(t.sum())
+        rg = plan.ranges[r]
+        layer = lambda z0: int((per_tile[:, :, z0] > 0).sum())   # noqa: E731
+        halo_tiles = (layer(mesh[2] - 2) if rg.upper >= 0 else 0) + \
+                     (layer(1 if rg.lower >= 0 else 0) if rg.lower >= 0 else 0)
+        fields = 2 * 19 * n_d * (n_fn if cfg.storage == "compact" else 64 * t_n)
+        meta = t_n * (364 + (76 if cfg.storage == "compact" else 0))
+        ranks.append({"rank": r, "z": [rg.z0, rg.z1], "tiles": t_n, "nonsolid_nodes": n_fn,
+                      "field_gb": round(fields / 1e9, 3), "metadata_gb": round(meta / 1e9, 3),
+                      "halo_bytes_sent_received_per_step": 2 * 80 * n_d * halo_tiles,
+                      "fits": (fields + meta) / 1e9 < budget_gb})
+    return {"world": world, "precision": precision, "storage": cfg.storage,
+            "table": cfg.table.value, "budget_gb": budget_gb, "ranks": ranks,
+            "fits": all(r["fits"] for r in ranks)}

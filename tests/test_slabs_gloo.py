@@ -132,3 +132,22 @@ def test_plan_balances_fluid_nodes():
     plan = SlabPlan(per, 4)
     assert plan.ranges[0].lower == 3 and plan.ranges[3].upper == 0
     assert plan.local_types(per.types, 0).shape[2] == 8 + 2 * TILE
+
+
+def test_plan_run_matches_decomposition():
+    """slabs.plan_run (host-only sizing) agrees with the slab plan and the
+    tile counts of the geometry."""
+    import numpy as np
+    from paper_1611_02445_b200 import geometry, slabs
+    geo = geometry.generate_channel("square", 12, axis=2, length=40, ends="periodic")
+    one = slabs.plan_run(geo, 1)
+    t = geo.types != 0
+    assert one["ranks"][0]["nonsolid_nodes"] == int(t.sum())
+    assert one["ranks"][0]["tiles"] == 3 * 3 * 10 and one["fits"]      # 12 x 12 -> 3 x 3 tiles
+    four = slabs.plan_run(geo, 4, precision="f32", storage="compact")
+    owned = sum(r["z"][1] - r["z"][0] for r in four["ranks"])
+    assert owned == 40 and four["storage"] == "compact"
+    # periodic z: every rank has two ghost layers and two boundary layers
+    assert all(r["tiles"] == 9 * ((r["z"][1] - r["z"][0]) // 4 + 2) for r in four["ranks"])
+    assert all(r["halo_bytes_sent_received_per_step"] == 2 * 80 * 4 * 18 for r in four["ranks"])
+    assert four["ranks"][0]["field_gb"] == round(2 * 19 * 4 * four["ranks"][0]["nonsolid_nodes"] / 1e9, 3)
