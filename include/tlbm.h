@@ -220,6 +220,15 @@ int tlbm_halo_compact(void *d_f, int dtype, int64_t tile_begin, int64_t tile_end
                       int pack, void *d_buf, const int64_t *d_base, const int32_t *d_nf,
                       const uint8_t *d_rank, void *stream);
 
+/* ---- geometry generation (csrc/generate.cu; geometry.py:200-269) -------- */
+/* For m sphere centres (3 doubles each, d_centres), every voxel of the n^3
+ * box (C order) covered by sphere i -- ((x+.5-c0)^2 + (y+.5-c1)^2) +
+ * (z+.5-c2)^2 <= radius^2 in float64 -- gets d_first = min(d_first,
+ * first_index + i); the host derives the reference's stopping sphere from
+ * the per-index counts (geometry.generate_sphere_pack(device=...)). */
+int tlbm_sphere_cover(const double *d_centres, int64_t first_index, int64_t m, int n,
+                      double radius, int32_t *d_first, void *stream);
+
 /* *d_counter += k (one thread; the last node of a captured step graph). */
 int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream);
 

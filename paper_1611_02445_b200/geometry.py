@@ -186,6 +186,54 @@ def generate_channel(shape, d, axis=0, offsets=(0, 0), length=16, ends="wall",
                     outlet_density=outlet_density, periodic=tuple(periodic))
 
 
+def _sphere_pack_device(n, r, target, seed, max_passes, device):
+    """Solid/fluid tags of the sphere pack, built on the GPU (see
+    generate_sphere_pack).  Same RNG stream, same stopping rule:
+    porosity(k) = 1 - solid(k) / n^3 with solid(k) the voxels whose first
+    covering sphere is among the pass's first k; the pass stops at the
+    smallest k with porosity(k) <= target + band and is accepted when
+    porosity(k) >= target - band, else the next pass starts at sphere k."""
+    import torch
+
+    from . import _native as nat
+    dev = nat.require_cuda(device)
+    band = 0.005
+    size = n * n * n
+    rng = np.random.default_rng(seed)
+    vol = 4.0 / 3.0 * np.pi * r ** 3
+    batch = int(max(64, 1.3 * np.log(1.0 / max(target, 1e-3)) * size / max(vol, 1.0) + 64))
+    drawn = np.empty((0, 3))
+    start = 0                      # first sphere of the current pass
+    big = np.iinfo(np.int32).max
+    first = torch.full((n, n, n), big, dtype=torch.int32, device=dev)
+    for _ in range(int(max_passes)):
+        first.fill_(big)
+        covered = start            # spheres of this pass already applied
+        k_stop = None
+        while k_stop is None:
+            if drawn.shape[0] < covered + batch:
+                drawn = np.concatenate([drawn, rng.uniform(0.0, n, size=(batch, 3))])
+            c = torch.from_numpy(np.ascontiguousarray(drawn[covered:covered + batch])).to(dev)
+            nat.call("tlbm_sphere_cover", nat.ptr(c), covered, batch, n, r, nat.ptr(first),
+                     nat.stream_ptr(dev))
+            covered += batch
+            idx = first[first < covered] - start
+            counts = torch.bincount(idx.to(torch.int64), minlength=covered - start)
+            solid = torch.cat([torch.zeros(1, dtype=torch.int64, device=dev),
+                               torch.cumsum(counts, 0)]).cpu().numpy()
+            porosity = 1.0 - solid / size
+            hit = np.flatnonzero(porosity <= target + band)
+            if hit.size:
+                k_stop = int(hit[0])
+        if porosity[k_stop] >= target - band:
+            solid_mask = (first < start + k_stop).cpu().numpy()
+            return np.where(solid_mask, np.uint8(NodeType.SOLID),
+                            np.uint8(NodeType.FLUID)).astype(np.uint8)
+        start += k_stop            # the next pass continues the RNG stream
+    raise ValueError(f"target porosity {target} unreachable within +/-{band} after "
+                     f"{max_passes} packing passes")
+
+
 def _type_box_faces(t, flow_axis):
     """Inlet/outlet on the two flow-axis faces, BB on the other four, walls
     winning shared edges (geometry.py:251-266)."""
@@ -203,7 +251,7 @@ def _type_box_faces(t, flow_axis):
 
 def generate_sphere_pack(n, diameter, target_porosity, seed, flow_axis=2,
                          inlet_velocity=(0.0, 0.0, 0.0), outlet_density=1.0,
-                         max_passes=20):
+                         max_passes=20, device=None):
     """Seeded overlapping solid spheres until porosity is within +/-0.005 of
     the target (geometry.py:200-269).
 
@@ -211,12 +259,21 @@ def generate_sphere_pack(n, diameter, target_porosity, seed, flow_axis=2,
     applies the same ``(x+0.5-c)^2 sums <= r^2`` test as the reference, but
     only inside each sphere's bounding box, keeping a running solid count;
     the resulting voxels are bit-identical (tests/test_geometry.py).
+
+    ``device`` (extension): build the pack on that CUDA device instead
+    (csrc/generate.cu) -- every voxel records its first covering sphere and
+    the stopping sphere follows from the per-sphere counts; same voxels.
     """
     n = int(n)
     if n < 4:
         raise ValueError(f"box edge must be at least 4 nodes, got {n}")
     if not 0.0 < target_porosity < 1.0:
         raise ValueError(f"target porosity must be in (0, 1): {target_porosity}")
+    if device is not None:
+        t = _sphere_pack_device(n, float(diameter) / 2.0, target_porosity, seed, max_passes,
+                                device)
+        _type_box_faces(t, flow_axis)
+        return Geometry(t, inlet_velocity=inlet_velocity, outlet_density=outlet_density)
     r = float(diameter) / 2.0
     rr = r * r
     band = 0.005

@@ -106,3 +106,20 @@ def test_rejects_bad_faces():
     t[0, 0, 0] = 9          # unknown tag
     with pytest.raises(ValueError):
         tiling.build_tiling(geo_mod.Geometry(t))
+
+
+@pytest.mark.parametrize("n,d,p,seed", [(64, 12, 0.5, 1234), (48, 10, 0.2, 7), (96, 20, 0.8, 3),
+                                        (20, 8, 0.5, 11), (16, 8, 0.6, 5)])
+def test_sphere_pack_on_device_bit_identical(n, d, p, seed):
+    """generate_sphere_pack(device=0) (csrc/generate.cu) == the host
+    generator (itself bit-identical to the reference), including packs whose
+    early passes overshoot the porosity band and restart."""
+    from paper_1611_02445_b200 import geometry
+    try:
+        host = geometry.generate_sphere_pack(n, d, p, seed, inlet_velocity=(0, 0, 0.01))
+    except ValueError:
+        with pytest.raises(ValueError):
+            geometry.generate_sphere_pack(n, d, p, seed, device=0)
+        return
+    dev = geometry.generate_sphere_pack(n, d, p, seed, inlet_velocity=(0, 0, 0.01), device=0)
+    assert np.array_equal(dev.types, host.types)
