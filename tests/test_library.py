@@ -135,3 +135,14 @@ def test_auto_storage_resolution():
     assert f32.storage == "blocks"
     with pytest.raises(ValueError):
         solver.SimulationConfig(storage="auto", table="xyz")
+
+
+def test_integration_stub_matches_binding():
+    """The StepArgs stub a tilelbm maintainer would copy from INTEGRATION.md
+    lists the same fields, in order, as the binding (and so the header)."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    block = text[text.index("class StepArgs(ctypes.Structure)"):]
+    block = block[:block.index("\n\n")]
+    names = re.findall(r'\("([a-z_0-9]+)",', block)
+    assert names == [f[0] for f in nat.StepArgs._fields_]
