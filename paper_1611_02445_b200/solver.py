@@ -140,10 +140,10 @@ class Solver:
         y-blocked order (traversal_order) when a z-layer of tiles moves more
         bytes than L2_REUSE_BUDGET, so that the 128-byte L2 lines a tile
         shares with its z neighbour are still resident when the neighbour
-        runs (fp32 512^3: 0.89 -> 0.93 of peak; 1024 x 1024 x 128: 0.83 ->
-        0.92).  fp64 blocks share no lines across z and lose DRAM streaming
-        locality in the blocked order (0.99 -> 0.94), so they keep the tile
-        order, as does compact storage (measured slower).  An int forces the
+        runs (fp32 512^3: +2-3% in a same-box A/B).  fp64 blocks share no
+        lines across z and lose DRAM streaming locality in the blocked order
+        (0.974 -> 0.945), so they keep the tile order, as does compact
+        storage (measured slower).  An int forces the
         blocking with that many tile rows."""
         self.config = config if config is not None else SimulationConfig()
         self.geometry = geometry
