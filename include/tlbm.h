@@ -229,6 +229,17 @@ int tlbm_halo_compact(void *d_f, int dtype, int64_t tile_begin, int64_t tile_end
 int tlbm_sphere_cover(const double *d_centres, int64_t first_index, int64_t m, int n,
                       double radius, int32_t *d_first, void *stream);
 
+/* Vessel tree (geometry.py:generate_vessel_tree): d_discs holds, for every
+ * z plane, nb slots of (cx, cy, r) of which the first d_count[z] are used; a
+ * voxel (x, y, z) of the nx*ny*nz box (C order) is lumen when margin <= x <
+ * nx - margin, margin <= y < ny - margin and (x-cx)^2 + (y-cy)^2 <= r^2 in
+ * float64 for some used disc (d_lumen, nx*ny*nz bytes of scratch).  d_types
+ * receives SOLID / BB_WALL / FLUID, with FLUID on z = 0 as VELOCITY_INLET and
+ * on z = nz-1 as PRESSURE_OUTLET (lumen with all six neighbours in the lumen
+ * is FLUID; x/y outside the box count as solid, z replicates the end planes). */
+int tlbm_vessel_tree(const double *d_discs, const int32_t *d_count, int nb, int nx, int ny,
+                     int nz, int margin, uint8_t *d_lumen, uint8_t *d_types, void *stream);
+
 /* *d_counter += k (one thread; the last node of a captured step graph). */
 int tlbm_advance_counter(int64_t *d_counter, int64_t k, void *stream);
 

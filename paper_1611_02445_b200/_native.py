@@ -74,6 +74,8 @@ _PROTOS = {
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),
     "tlbm_step": (c_int, [ctypes.POINTER(StepArgs), c_vp]),
     "tlbm_advance_counter": (c_int, [c_vp, c_i64, c_vp]),
+    "tlbm_vessel_tree": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp,
+                                 c_vp]),
     "tlbm_compact_ranks": (c_int, [c_vp, c_i64, c_vp, c_vp]),
     "tlbm_sphere_cover": (c_int, [c_vp, c_i64, c_i64, c_int, c_dbl, c_vp, c_vp]),
     "tlbm_halo_compact": (c_int, [c_vp, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,

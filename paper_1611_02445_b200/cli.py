@@ -26,7 +26,7 @@ class UsageError(ValueError):
 
 
 def parse_geometry(spec):
-    from . import geometry as g
+    from . import geometry as g, workloads
     kind, _, rest = spec.partition(":")
     a = rest.split(":") if rest else []
     try:
@@ -41,11 +41,13 @@ def parse_geometry(spec):
                                       inlet_velocity=(0.01, 0.0, 0.0))
         if kind == "spheres":
             return g.generate_sphere_pack(int(a[0]), float(a[1]), float(a[2]), int(a[3]),
-                                          inlet_velocity=(0.0, 0.0, 0.01))
+                                          inlet_velocity=(0.0, 0.0, 0.01),
+                                          device=workloads.generator_device())
         if kind == "box":
             return g.generate_box(int(a[0]), inlet_velocity=(0.0, 0.0, 0.01))
         if kind == "vessel":
-            return g.generate_vessel_tree(tuple(int(v) for v in a[:3]))
+            return g.generate_vessel_tree(tuple(int(v) for v in a[:3]),
+                                          device=workloads.generator_device())
         if kind == "file":
             return g.load_voxels_path(rest)
     except (IndexError, ValueError) as exc:

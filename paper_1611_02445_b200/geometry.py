@@ -17,6 +17,8 @@ Extensions over the reference (all documented in DESIGN.md):
 * ``generate_box`` -- the porosity-1.0 end of the sphere-pack sweep, which
   ``generate_sphere_pack`` rejects (geometry.py:218-219).
 * ``generate_vessel_tree`` -- seeded bifurcating-tube geometry for config 4.
+* ``device=`` on both generators builds the voxels on the GPU
+  (csrc/generate.cu), bit-identical to the host path.
 * ``generate_sphere_pack`` draws the identical random sequence as the
   reference but rasterises each sphere only inside its bounding box, so the
   result is bit-identical and O(d^3) per sphere instead of O(n^3).
@@ -332,7 +334,7 @@ def generate_box(n, flow_axis=2, inlet_velocity=(0.0, 0.0, 0.0),
 
 def generate_vessel_tree(shape=(512, 512, 1024), levels=3, root_radius=None,
                          seed=1234, wiggle=0.06, inlet_velocity=(0.0, 0.0, 0.01),
-                         outlet_density=1.0):
+                         outlet_density=1.0, device=None):
     """Seeded tortuous bifurcating tube tree along +z (BASELINE config 4).
 
     A root tube enters at the centre of the z=0 face and bifurcates ``levels``
@@ -344,6 +346,11 @@ def generate_vessel_tree(shape=(512, 512, 1024), levels=3, root_radius=None,
     z=nz-1 PRESSURE_OUTLET.  Tubes keep a margin from the x/y faces, so every
     inlet/outlet node lies on exactly one domain face.  Built slice by slice
     in O(nx*ny*nz) time.
+
+    ``device`` (extension): rasterise and classify on that CUDA device
+    (csrc/generate.cu) from the same per-slice branch discs; bit-identical
+    voxels, a few hundred milliseconds instead of tens of seconds at
+    1024x1024x2048.
     """
     nx, ny, nz = (int(v) for v in shape)
     rng = np.random.default_rng(seed)
@@ -385,10 +392,16 @@ def generate_vessel_tree(shape=(512, 512, 1024), levels=3, root_radius=None,
         wy = amp * np.sin(2 * np.pi * z / lam[lev][i] + ph[1])
         return cx0 + px + wx, cy0 + py + wy, r
 
+    margin = 2.0
+    if device is not None:
+        t = _vessel_device(nx, ny, nz, [
+            [centre(min(levels, int(z // seg)), i, float(z))
+             for i in range(len(tree[min(levels, int(z // seg))]))] for z in range(nz)],
+            int(margin), device)
+        return Geometry(t, inlet_velocity=inlet_velocity, outlet_density=outlet_density)
     X = np.arange(nx, dtype=np.float64)[:, None]
     Y = np.arange(ny, dtype=np.float64)[None, :]
     lumen = np.zeros((nx, ny, nz), dtype=bool)
-    margin = 2.0
     for z in range(nz):
         lev = min(levels, int(z // seg))
         sl = lumen[:, :, z]
@@ -418,6 +431,27 @@ def generate_vessel_tree(shape=(512, 512, 1024), levels=3, root_radius=None,
     f1[f1 == NodeType.FLUID] = NodeType.PRESSURE_OUTLET
     return Geometry(t, inlet_velocity=inlet_velocity,
                     outlet_density=outlet_density)
+
+
+def _vessel_device(nx, ny, nz, discs, margin, device):
+    """Vessel-tree tags on the GPU from per-slice (cx, cy, r) discs."""
+    import torch
+
+    from . import _native as nat
+    dev = nat.require_cuda(device)
+    nb = max(len(d) for d in discs)
+    arr = np.zeros((nz, nb, 3))
+    for z, d in enumerate(discs):
+        if d:
+            arr[z, :len(d)] = d
+    d_discs = torch.from_numpy(arr).to(dev)
+    d_count = torch.tensor([len(d) for d in discs], dtype=torch.int32, device=dev)
+    lumen = torch.empty((nx, ny, nz), dtype=torch.uint8, device=dev)
+    types = torch.empty_like(lumen)
+    nat.call("tlbm_vessel_tree", nat.ptr(d_discs), nat.ptr(d_count), nb, nx, ny, nz, margin,
+             nat.ptr(lumen), nat.ptr(types), nat.stream_ptr(dev))
+    del lumen
+    return types.cpu().numpy()
 
 
 def save_voxels(geometry, stream):

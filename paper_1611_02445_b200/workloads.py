@@ -37,15 +37,24 @@ def channel_z(n=256, length=None):
                                      ends="periodic")
 
 
-def sphere_pack(porosity, n=256, diameter=40, seed=1234):
+def generator_device(device="auto"):
+    """The device the geometry generators run on: "auto" = cuda:0 when a GPU
+    is present (bit-identical voxels either way), None = the host."""
+    if device == "auto":
+        return 0 if torch.cuda.is_available() else None
+    return device
+
+
+def sphere_pack(porosity, n=256, diameter=40, seed=1234, device="auto"):
     if porosity >= 1.0:
         return geometry.generate_box(n, flow_axis=2, inlet_velocity=(0.0, 0.0, 0.01))
     return geometry.generate_sphere_pack(n, diameter, porosity, seed, flow_axis=2,
-                                         inlet_velocity=(0.0, 0.0, 0.01), outlet_density=1.0)
+                                         inlet_velocity=(0.0, 0.0, 0.01), outlet_density=1.0,
+                                         device=generator_device(device))
 
 
-def vessel_tree(shape=(512, 512, 1024), seed=1234):
-    return geometry.generate_vessel_tree(shape, seed=seed)
+def vessel_tree(shape=(512, 512, 1024), seed=1234, device="auto"):
+    return geometry.generate_vessel_tree(shape, seed=seed, device=generator_device(device))
 
 
 def perturbed_fields(t_n, dtype, device, u0=(0.04, 0.0, 0.0), amp=1e-3, seed=1234):

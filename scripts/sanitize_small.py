@@ -10,6 +10,8 @@ from paper_1611_02445_b200 import _native as nat  # noqa: E402
 from paper_1611_02445_b200 import collision, geometry, slabs, solver  # noqa: E402
 
 geo = geometry.generate_sphere_pack(20, 6, 0.6, seed=3, inlet_velocity=(0, 0, 0.02))
+assert (geometry.generate_sphere_pack(20, 6, 0.6, seed=3, inlet_velocity=(0, 0, 0.02),
+                                      device=0).types == geo.types).all()
 for prec in ("f64", "f32"):
     for fluid in ("incompressible", "quasi-compressible"):
         s = solver.Solver(geo, solver.SimulationConfig(precision=prec, fluid=fluid))

@@ -123,3 +123,17 @@ def test_sphere_pack_on_device_bit_identical(n, d, p, seed):
         return
     dev = geometry.generate_sphere_pack(n, d, p, seed, inlet_velocity=(0, 0, 0.01), device=0)
     assert np.array_equal(dev.types, host.types)
+
+
+@pytest.mark.parametrize("shape,levels,seed", [
+    ((40, 36, 64), 3, 1), ((33, 47, 29), 2, 5), ((24, 24, 1), 0, 2), ((64, 64, 96), 1, 9),
+    ((16, 20, 7), 3, 11)])
+def test_vessel_tree_on_device_bit_identical(shape, levels, seed):
+    """generate_vessel_tree(device=0) (csrc/generate.cu) == the host builder:
+    same lumen discs, walls, inlet and outlet planes."""
+    from paper_1611_02445_b200 import geometry
+    host = geometry.generate_vessel_tree(shape, levels=levels, seed=seed)
+    dev = geometry.generate_vessel_tree(shape, levels=levels, seed=seed, device=0)
+    assert np.array_equal(dev.types, host.types)
+    assert dev.inlet_velocity == host.inlet_velocity
+    assert (host.types == geometry.NodeType.VELOCITY_INLET).any() or shape[2] == 1
