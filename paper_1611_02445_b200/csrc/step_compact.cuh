@@ -64,9 +64,10 @@ __device__ const CompactPull kCompactPull = make_compact_pull();
 template <class T>
 constexpr int compact_tiles_per_cta() { return sizeof(T) == 4 ? 1 : TLBM_TPC_COMPACT; }
 
-template <class T, bool MRT, int VARIANT>
+template <class T, bool MRT, int VARIANT, bool FMA = false>
 constexpr int min_blocks_compact() {
-    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32 : TLBM_WARPS_MRT)
+    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32
+                                  : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
                 : (sizeof(T) == 4 ? TLBM_WARPS_COMPACT_F32 : TLBM_WARPS_COMPACT)) /
            (2 * compact_tiles_per_cta<T>());
 }
@@ -78,7 +79,7 @@ constexpr int min_blocks_compact() {
 // pointer per pull.  Otherwise 64-bit block pointers are staged.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32,
           bool ORDERED, bool HALO>
-__global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT>())
+__global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT, FMA>())
 step_kernel_compact(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
     __shared__ const T *s_src[OFF32 ? 1 : TPC][NBR];
@@ -158,7 +159,7 @@ step_kernel_compact(const StepParams<T, MRT> p) {
                 if constexpr (MRT && FMA)
                     status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
                 else if constexpr (MRT)
-                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
                 else if constexpr (FMA)
                     status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
                 else

@@ -15,6 +15,7 @@
 // (4 B/node meta word + 108 B/tile neighbour row).
 #pragma once
 #include <cmath>
+#include <cstring>
 
 #include "common.cuh"
 #include "physics.cuh"
@@ -23,9 +24,11 @@ namespace tlbm {
 namespace step_detail {
 
 // the MRT operator travels by value in the kernel parameters (constant bank)
+// (dense row-major A, or per-column distinct values when grouped: physics.cuh)
 template <class T, bool MRT>
 struct MrtOperator {
     T op[Q * Q];
+    int grouped;
 };
 template <class T>
 struct MrtOperator<T, false> {};
@@ -99,8 +102,14 @@ constexpr int TILE_VALUES = Q * 64;
 #ifndef TLBM_WARPS_F32
 #define TLBM_WARPS_F32 64
 #endif
+// MRT, reference arithmetic (grouped product, 19 live row sums): 16 warps/SM
+// at 126 registers, 1.054 ms vs 1.083 at 20 (160 B spill) and 1.182 at 24;
+// FMA arithmetic keeps 20 (scripts/exp/exp34.sh)
 #ifndef TLBM_WARPS_MRT
-#define TLBM_WARPS_MRT 20
+#define TLBM_WARPS_MRT 16
+#endif
+#ifndef TLBM_WARPS_MRT_FMA
+#define TLBM_WARPS_MRT_FMA 20
 #endif
 #ifndef TLBM_WARPS_MRT_F32
 #define TLBM_WARPS_MRT_F32 32
@@ -117,12 +126,12 @@ constexpr int tiles_per_cta() { return sizeof(T) == 4 ? TLBM_TPC_F32 : TLBM_TPC;
 #ifndef TLBM_WARPS_PROP_F32
 #define TLBM_WARPS_PROP_F32 48
 #endif
-template <class T, bool MRT, int VARIANT>
+template <class T, bool MRT, int VARIANT, bool FMA = false>
 constexpr int min_blocks() {
     constexpr int warps = sizeof(T) == 4
         ? (MRT ? TLBM_WARPS_MRT_F32
                : (VARIANT == TLBM_PROPAGATION_ONLY ? TLBM_WARPS_PROP_F32 : TLBM_WARPS_F32))
-        : (MRT ? TLBM_WARPS_MRT : TLBM_WARPS);
+        : (MRT ? (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT) : TLBM_WARPS);
     return warps / (2 * tiles_per_cta<T>());
 }
 
@@ -211,7 +220,7 @@ __device__ const PullTable kPullTables[3] = {make_pull_table<0>(), make_pull_tab
 // the 27 neighbour block addresses themselves and selects a pointer per pull.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool REL32, bool MRT, bool HALO,
           bool FMA, bool ORDERED>
-__global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, VARIANT>())
+__global__ void __launch_bounds__(64 * TPC, min_blocks<T, MRT, VARIANT, FMA>())
 step_kernel(const StepParams<T, MRT> p) {
     __shared__ int s_nbr[TPC][NBR];
     __shared__ const T *s_ptr[REL32 ? 1 : TPC][NBR];
@@ -286,7 +295,7 @@ step_kernel(const StepParams<T, MRT> p) {
                 if constexpr (MRT && FMA)
                     status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
                 else if constexpr (MRT)
-                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
                 else if constexpr (FMA)
                     status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
                 else
@@ -455,8 +464,24 @@ int launch_compact(const tlbm_step_args *a, cudaStream_t s) {
 
 template <class T, bool MRT, bool FMA>
 void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
-    if constexpr (MRT)
-        for (int k = 0; k < Q * Q; ++k) p.mrt.op[k] = T(a->mrt_op[k]);   // op.astype(dtype)
+    if constexpr (MRT) {
+        // op.astype(dtype); grouped when every column's equal-value rows of
+        // the compiled pattern hold bitwise-equal coefficients
+        bool grouped = !FMA && TLBM_MRT_GROUPED;
+        for (int i = 0; i < Q && grouped; ++i)
+            for (int j = 0; j < Q && grouped; ++j) {
+                const T c = T(a->mrt_op[i * Q + j]);
+                const T rep = T(a->mrt_op[mrt_rep(mrt_offset(j) + mrt_group(i, j)) * Q + j]);
+                grouped = memcmp(&c, &rep, sizeof(T)) == 0;
+            }
+        p.mrt.grouped = grouped;
+        if (grouped)
+            for (int j = 0; j < Q; ++j)
+                for (int k = 0; k < mrt_count(j); ++k)
+                    p.mrt.op[mrt_offset(j) + k] = T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]);
+        else
+            for (int k = 0; k < Q * Q; ++k) p.mrt.op[k] = T(a->mrt_op[k]);
+    }
     p.src = static_cast<const T *>(a->f_src);
     p.dst = static_cast<T *>(a->f_dst);
     p.nbr = a->nbr;

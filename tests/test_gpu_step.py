@@ -308,6 +308,40 @@ def test_mrt_random_geometries(c_oracle, seed):
             compare(s, o.f, dt)
 
 
+@pytest.mark.parametrize("case", ["tau0.537", "tau2.9", "broken", "rates"])
+def test_mrt_grouped_and_dense_products(c_oracle, case):
+    """The step runs the grouped MRT product when the operator has the
+    compiled column pattern (csrc/mrt_pattern.cuh) and the dense one when it
+    does not (one perturbed coefficient, custom moment rates); both bit-exact
+    vs the oracle, both storages."""
+    rng = np.random.default_rng(77)
+    shape = (14, 11, 17)
+    t = random_geometry(rng, shape)
+    geo = geometry.Geometry(t, inlet_velocity=(0.0, 0.01, 0.02), outlet_density=1.0)
+    tau = {"tau0.537": 0.537, "tau2.9": 2.9}.get(case, 0.6)
+    rates = None
+    op = None
+    if case == "broken":
+        op = solver.SimulationConfig(collision="mrt", tau=tau).mrt_operator.copy()
+        op[4, 0] = np.nextafter(op[4, 0], 1.0)
+    if case == "rates":
+        rates = np.random.default_rng(3).uniform(0.8, 1.9, 19)
+    for dt in (np.float64, np.float32):
+        m = MODELS["inc"]
+        for storage in ("blocks", "compact"):
+            cfg = solver.SimulationConfig(collision="mrt", fluid=m, tau=tau, storage=storage,
+                                          precision="f64" if dt == np.float64 else "f32",
+                                          u_max_guard=0.0, mrt_relaxation=rates, mrt_matrix=op)
+            f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), 9)
+            o = c_oracle.DenseOracle(t, m, tau, geo.inlet_velocity, 1.0, f0=f0, dtype=dt,
+                                     mrt_operator=cfg.mrt_operator.astype(dt))
+            o.run(6)
+            s = solver.Solver(geo, cfg)
+            s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+            s.step(6)
+            compare(s, o.f, dt)
+
+
 def test_mrt_bgk_limit():
     """SPEC acceptance 9: all moment rates = 1/tau -> MRT == LBGK to 1e-12."""
     geo = geometry.generate_sphere_pack(24, 6, 0.6, seed=8, inlet_velocity=(0, 0, 0.01))

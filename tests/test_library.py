@@ -146,3 +146,26 @@ def test_integration_stub_matches_binding():
     block = block[:block.index("\n\n")]
     names = re.findall(r'\("([a-z_0-9]+)",', block)
     assert names == [f[0] for f in nat.StepArgs._fields_]
+
+
+def test_mrt_pattern_header_is_current():
+    """csrc/mrt_pattern.cuh (the grouped MRT product's column pattern) is what
+    scripts/gen_mrt_pattern.py derives from the current operator, and every
+    row/column it groups holds bitwise-equal default-operator coefficients."""
+    import importlib.util
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location(
+        "gen_mrt_pattern", os.path.join(root, "scripts", "gen_mrt_pattern.py"))
+    gen = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(gen)
+    assert open(gen.OUT).read() == gen.render()
+    from paper_1611_02445_b200 import collision
+    txt = gen.render()
+    pat = np.array([[int(v) for v in r.split(",")]
+                    for r in re.findall(r"\{([0-9, ]+)\},", txt)])
+    assert pat.shape == (19, 19)
+    for tau in (0.6, 0.9, 1.7):
+        op = collision.mrt_operator(collision.default_mrt_rates(tau))
+        for j in range(19):
+            for g in set(pat[:, j]):
+                assert len({op[i, j].tobytes() for i in np.flatnonzero(pat[:, j] == g)}) == 1
