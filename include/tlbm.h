@@ -41,10 +41,12 @@ enum { TLBM_OK = 0, TLBM_ERR_ARG = 1, TLBM_ERR_CUDA = 2 };
 /* step variants (SPEC.md:531-539 bench ladder) */
 enum { TLBM_FULL = 0, TLBM_PROPAGATION_ONLY = 1, TLBM_READ_WRITE_ONLY = 2 };
 /* collision arithmetic of the step: REFERENCE keeps numpy's unfused operation
- * order (bit-identical to the reference); FMA contracts the equilibrium,
- * relaxation and MRT operator products into fused multiply-adds (fewer
- * instructions; parity within the stated 1e-12 tolerance).  FMA is fp64-only:
- * in fp32 it drifts past the 1e-5 bar (u: 1.1e-5 after 1000 cavity steps). */
+ * order (bit-identical to the reference); FMA contracts the equilibrium and
+ * relaxation products into fused multiply-adds and applies an MRT operator of
+ * the form M^-1 diag(s) M (s = 0 on the conserved moments) in moment space
+ * (fewer instructions; parity within the stated 1e-12 tolerance); any other
+ * MRT operator runs in reference arithmetic.  FMA is fp64-only: in fp32 it
+ * drifts past the 1e-5 bar (u: 1.1e-5 after 1000 cavity steps). */
 enum { TLBM_ARITH_REFERENCE = 0, TLBM_ARITH_FMA = 1 };
 /* bits of the device status word written by tlbm_step / tlbm_macroscopic */
 enum { TLBM_FLAG_DIVERGED = 1, TLBM_FLAG_GUARD = 2 };

@@ -99,8 +99,8 @@ __device__ __forceinline__ T feq_of(int q, T rho, T br) {
 //   bracket(q), bracket(opp q) = fma(+-3, cu, fma(4.5 cu, cu, -1.5 usq))
 //   feq = fma(w, bracket, w rho)            (quasi: fma(w rho, bracket, w rho))
 //   g  <- fma(1/tau, feq - g, g)
-//   MRT rows: acc = fma(A_ij, d_j, acc)
-// 149 instead of 216 FP instructions per LBGK node and 361 instead of 722 for
+//   MRT: the operator applied in moment space (collide_mrt_fma below)
+// 149 instead of 216 FP instructions per LBGK node and 218 instead of 722 for
 // the MRT operator.  Every FMA rounds once where the reference rounds twice,
 // so results differ from the reference in the last bits only; the parity bar
 // is the stated 1e-12 tolerance (tests/test_gpu_fma.py: 2.7e-15 in f, 2.0e-14
@@ -157,16 +157,110 @@ __device__ __forceinline__ uint32_t collide_fma(T (&g)[Q], T inv_tau, T guard_sq
     return st;
 }
 
+// The D3Q19 moment basis of collision.py (MOMENT_MATRIX, collision.py:150-
+// 160): integer coefficients of moment k on direction q.
+__host__ __device__ constexpr int moment_coef(int k, int q) {
+    const int x = ex(q), y = ey(q), z = ez(q);
+    const int e2 = x * x + y * y + z * z;
+    const int axx = 3 * x * x - e2, aww = y * y - z * z;
+    switch (k) {
+        case 0: return 1;
+        case 1: return 19 * e2 - 30;
+        case 2: return (21 * e2 * e2 - 53 * e2 + 24) / 2;
+        case 3: return x;
+        case 4: return (5 * e2 - 9) * x;
+        case 5: return y;
+        case 6: return (5 * e2 - 9) * y;
+        case 7: return z;
+        case 8: return (5 * e2 - 9) * z;
+        case 9: return axx;
+        case 10: return (3 * e2 - 5) * axx;
+        case 11: return aww;
+        case 12: return (3 * e2 - 5) * aww;
+        case 13: return x * y;
+        case 14: return y * z;
+        case 15: return x * z;
+        case 16: return aww * x;
+        case 17: return (z * z - x * x) * y;
+        default: return (x * x - y * y) * z;
+    }
+}
+// moments of odd degree flip sign between q and opp(q)
+__host__ __device__ constexpr bool moment_odd(int k) {
+    return (k >= 3 && k <= 8) || k >= 16;
+}
+__host__ __device__ constexpr bool moment_conserved(int k) {
+    return k == 0 || k == 3 || k == 5 || k == 7;
+}
+__host__ __device__ constexpr int moment_norm(int k) {
+    int n = 0;
+    for (int q = 0; q < Q; ++q) n += moment_coef(k, q) * moment_coef(k, q);
+    return n;
+}
+
+// A coefficient-times-term with an integer coefficient: +-1 as add/sub, 0
+// skipped, otherwise one FMA; the first term starts the sum.
+template <class T>
+__device__ __forceinline__ void acc_int(T &acc, bool &first, int c, T v) {
+    if (c == 0) return;
+    if (first) {
+        acc = c == 1 ? v : c == -1 ? -v : T(c) * v;
+        first = false;
+    } else {
+        acc = c == 1 ? acc + v : c == -1 ? acc - v : fmad(T(c), v, acc);
+    }
+}
+
+// MRT in FMA arithmetic, in moment space: the operator is M^-1 diag(s) M in
+// collision.py's basis with s = 0 on the conserved moments (the host checks
+// that form, step_impl.cuh: mrt_moment_rates, and runs reference arithmetic
+// for any other operator); w[k] = s_k / |M_k|^2.  Direction pairs split into
+// sums (even moments) and differences (odd moments): 18 pair terms, 15
+// projections with integer coefficients (83 add / FMA), 15 scalings, the
+// transpose back (83) and 19 recombinations -- 218 DP instructions per node
+// instead of the 380 of the dense FMA product.
 template <class T, int QUASI>
-__device__ __forceinline__ uint32_t collide_mrt_fma(T (&g)[Q], const T *op, T guard_sq) {
+__device__ __forceinline__ uint32_t collide_mrt_fma(T (&g)[Q], const T *w, T guard_sq) {
     T d[Q];
     const uint32_t st = deviations_fma<T, QUASI>(g, d, guard_sq);
+    T sp[Q], dp[Q];
 #pragma unroll
-    for (int i = 0; i < Q; ++i) {
-        T acc = op[i * Q] * d[0];
+    for (int q = 1; q < Q; ++q) {
+        if (opp(q) < q) continue;
+        sp[q] = d[q] + d[opp(q)];
+        dp[q] = d[q] - d[opp(q)];
+    }
+    T y[Q];
 #pragma unroll
-        for (int j = 1; j < Q; ++j) acc = fmad(op[i * Q + j], d[j], acc);
-        g[i] = g[i] + acc;
+    for (int k = 0; k < Q; ++k) {
+        if (moment_conserved(k)) continue;
+        T m = T(0);
+        bool first = true;
+        if (!moment_odd(k)) acc_int(m, first, moment_coef(k, 0), d[0]);
+#pragma unroll
+        for (int q = 1; q < Q; ++q) {
+            if (opp(q) < q) continue;
+            acc_int(m, first, moment_coef(k, q), moment_odd(k) ? dp[q] : sp[q]);
+        }
+        y[k] = w[k] * m;
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (q > 0 && opp(q) < q) continue;
+        T ev = T(0), od = T(0);
+        bool fe = true, fo = true;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            if (moment_conserved(k)) continue;
+            if (moment_odd(k)) acc_int(od, fo, moment_coef(k, q), y[k]);
+            else acc_int(ev, fe, moment_coef(k, q), y[k]);
+        }
+        if (q == 0) {
+            g[0] = g[0] + ev;
+        } else {
+            g[q] = g[q] + (ev + od);
+            g[opp(q)] = g[opp(q)] + (ev - od);
+        }
     }
     return st;
 }

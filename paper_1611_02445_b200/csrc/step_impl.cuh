@@ -14,6 +14,7 @@
 // tile, so DRAM traffic is the 2 x 19 x 8 B / node minimum plus metadata
 // (4 B/node meta word + 108 B/tile neighbour row).
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -28,7 +29,7 @@ namespace step_detail {
 template <class T, bool MRT>
 struct MrtOperator {
     T op[Q * Q];
-    int grouped;
+    int grouped;   // reference arithmetic: per-column distinct values
 };
 template <class T>
 struct MrtOperator<T, false> {};
@@ -109,7 +110,7 @@ constexpr int TILE_VALUES = Q * 64;
 #define TLBM_WARPS_MRT 16
 #endif
 #ifndef TLBM_WARPS_MRT_FMA
-#define TLBM_WARPS_MRT_FMA 20
+#define TLBM_WARPS_MRT_FMA 24
 #endif
 #ifndef TLBM_WARPS_MRT_F32
 #define TLBM_WARPS_MRT_F32 32
@@ -353,11 +354,20 @@ int launch_halo(const tlbm_step_args *a, cudaStream_t s) {
     return launch_as<T, QUASI, TABLE, VARIANT, REL32, MRT, false, FMA>(a, s);
 }
 
-// FMA arithmetic is fp64-only (tlbm_step rejects it for fp32)
+inline bool mrt_moment_rates(const double *A, double *w);
+
+// FMA arithmetic is fp64-only (tlbm_step rejects it for fp32).  An MRT
+// operator that is not M^-1 diag(s) M (custom matrix) runs in reference
+// arithmetic: bit-exact, so inside the FMA tolerance too.
+inline bool fma_path(const tlbm_step_args *a, bool mrt) {
+    double w[Q];
+    return a->arith == TLBM_ARITH_FMA && (!mrt || mrt_moment_rates(a->mrt_op, w));
+}
+
 template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT>
 int launch_arith(const tlbm_step_args *a, cudaStream_t s) {
     constexpr bool kFma = VARIANT == TLBM_FULL && sizeof(T) == 8;
-    if (kFma && a->arith == TLBM_ARITH_FMA)
+    if (kFma && fma_path(a, MRT))
         return launch_halo<T, QUASI, TABLE, VARIANT, REL32, MRT, kFma>(a, s);
     return launch_halo<T, QUASI, TABLE, VARIANT, REL32, MRT, false>(a, s);
 }
@@ -457,16 +467,65 @@ int launch_compact(const tlbm_step_args *a, cudaStream_t s) {
         return TLBM_ERR_ARG;
     }
     constexpr bool kFma = VARIANT == TLBM_FULL && sizeof(T) == 8;
-    if (kFma && a->arith == TLBM_ARITH_FMA)
+    if (kFma && fma_path(a, MRT))
         return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, kFma>(a, s);
     return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, false>(a, s);
+}
+
+// Is A = M^-1 diag(s) M in the collision.py moment basis, with s = 0 on the
+// conserved moments?  B = M A M^T D^-1 must be diagonal to 1e-12 of its
+// largest entry; then w[k] = s_k / |M_k|^2 (FMA-arithmetic moment path).
+inline bool mrt_moment_rates_uncached(const double *A, double *w) {
+    double MA[Q][Q];
+    for (int k = 0; k < Q; ++k)
+        for (int r = 0; r < Q; ++r) {
+            double acc = 0.0;
+            for (int q = 0; q < Q; ++q) acc += moment_coef(k, q) * A[q * Q + r];
+            MA[k][r] = acc;
+        }
+    double B[Q][Q], big = 0.0;
+    for (int k = 0; k < Q; ++k)
+        for (int l = 0; l < Q; ++l) {
+            double acc = 0.0;
+            for (int r = 0; r < Q; ++r) acc += MA[k][r] * moment_coef(l, r);
+            B[k][l] = acc / moment_norm(l);
+            big = std::max(big, std::fabs(B[k][l]));
+        }
+    const double tol = 1e-12 * std::max(big, 1.0);
+    for (int k = 0; k < Q; ++k) {
+        for (int l = 0; l < Q; ++l)
+            if (l != k && !(std::fabs(B[k][l]) <= tol)) return false;
+        if (moment_conserved(k) && !(std::fabs(B[k][k]) <= tol)) return false;
+        w[k] = moment_conserved(k) ? 0.0 : B[k][k] / moment_norm(k);
+    }
+    return true;
+}
+
+inline bool mrt_moment_rates(const double *A, double *w) {
+    // per-thread memo of the last operator (fill_params runs every launch)
+    thread_local double last_A[Q * Q], last_w[Q];
+    thread_local bool last_ok = false, have = false;
+    if (have && memcmp(last_A, A, sizeof(last_A)) == 0) {
+        memcpy(w, last_w, sizeof(last_w));
+        return last_ok;
+    }
+    have = false;
+    memcpy(last_A, A, sizeof(last_A));
+    last_ok = mrt_moment_rates_uncached(A, last_w);
+    have = true;
+    memcpy(w, last_w, sizeof(last_w));
+    return last_ok;
 }
 
 template <class T, bool MRT, bool FMA>
 void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     if constexpr (MRT) {
         // op.astype(dtype); grouped when every column's equal-value rows of
-        // the compiled pattern hold bitwise-equal coefficients
+        // the compiled pattern hold bitwise-equal coefficients; in FMA
+        // arithmetic, moment space when op = M^-1 diag(s) M
+        double w[Q];
+        if (FMA && !mrt_moment_rates(a->mrt_op, w))   // launch_arith routes these
+            for (int k = 0; k < Q; ++k) w[k] = 0.0;   // to reference arithmetic
         bool grouped = !FMA && TLBM_MRT_GROUPED;
         for (int i = 0; i < Q && grouped; ++i)
             for (int j = 0; j < Q && grouped; ++j) {
@@ -475,7 +534,9 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
                 grouped = memcmp(&c, &rep, sizeof(T)) == 0;
             }
         p.mrt.grouped = grouped;
-        if (grouped)
+        if (FMA)
+            for (int k = 0; k < Q; ++k) p.mrt.op[k] = T(w[k]);
+        else if (grouped)
             for (int j = 0; j < Q; ++j)
                 for (int k = 0; k < mrt_count(j); ++k)
                     p.mrt.op[mrt_offset(j) + k] = T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]);

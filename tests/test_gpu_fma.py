@@ -119,3 +119,36 @@ def test_fma_close_to_reference_arithmetic():
             runs.append(s.fields_canonical()[:, s.nonsolid_mask()])
         assert rel(runs[1], runs[0]) <= TOL[dt]
         assert not np.array_equal(runs[1], runs[0])    # the FMA kernel really ran
+
+
+@pytest.mark.parametrize("case", ["default", "rates", "custom_matrix"])
+def test_mrt_fma_moment_space_and_fallback(c_oracle, case):
+    """FMA-arithmetic MRT runs in moment space when the operator is
+    M^-1 diag(s) M with s = 0 on the conserved moments (default and custom
+    rates: within the tolerance, and not bitwise the reference), and in
+    reference arithmetic otherwise (a custom matrix: bit-exact)."""
+    rng = np.random.default_rng(31)
+    shape = (15, 12, 18)
+    t = random_geometry(rng, shape)
+    geo = geometry.Geometry(t, inlet_velocity=(0.0, 0.01, 0.02), outlet_density=1.0)
+    rates = None
+    if case == "rates":
+        rates = np.random.default_rng(4).uniform(0.7, 1.95, 19)
+        rates[[0, 3, 5, 7]] = 0.0
+    cfg0 = solver.SimulationConfig(collision="mrt", tau=0.6, mrt_relaxation=rates)
+    op = cfg0.mrt_operator.copy()
+    if case == "custom_matrix":
+        op[4, 0] *= 1.0 + 1e-9
+    dt = np.float64
+    for m in MODELS.values():
+        for storage in ("blocks", "compact"):
+            f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), 5)
+            want = oracle_run(c_oracle, geo, m, dt, f0, 25, mrt_operator=op)
+            cfg = solver.SimulationConfig(collision="mrt", fluid=m, tau=0.6, u_max_guard=0.0,
+                                          mrt_matrix=op, arithmetic="fma", storage=storage)
+            s = solver.Solver(geo, cfg)
+            s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
+            s.step(25)
+            exact = case == "custom_matrix"
+            r_f, _, _ = compare(s, want, dt, exact=exact)
+            assert exact or r_f > 0.0      # the moment-space kernel really ran
