@@ -383,9 +383,11 @@ int launch(const tlbm_step_args *a, cudaStream_t s) {
         set_error("tlbm_step: compact storage needs the xyz layout table");
         return TLBM_ERR_ARG;
     }
-    if (VARIANT == TLBM_FULL && a->collision == TLBM_MRT) {
-        if (a->rel32) return launch_arith<T, QUASI, TABLE, VARIANT, true, true>(a, s);
-        return launch_arith<T, QUASI, TABLE, VARIANT, false, true>(a, s);
+    if constexpr (VARIANT == TLBM_FULL) {     // MRT kernels only for the full step
+        if (a->collision == TLBM_MRT) {
+            if (a->rel32) return launch_arith<T, QUASI, TABLE, VARIANT, true, true>(a, s);
+            return launch_arith<T, QUASI, TABLE, VARIANT, false, true>(a, s);
+        }
     }
     if (a->rel32)
         return launch_arith<T, QUASI, TABLE, VARIANT, true, false>(a, s);
