@@ -102,3 +102,19 @@ def test_cli_runtime_error_exit_code(capsys):
     and a one-line message (no traceback)."""
     assert cli.main(["run", "--geometry", "cavity:8", "--precision", "f32", "--arith", "fma"]) == 5
     assert "f64-only" in capsys.readouterr().err
+
+
+def test_geometry_generators_run_on_the_host_without_a_gpu():
+    """workloads / CLI pick the GPU generators only when a GPU is present;
+    without one the host builders run (same voxels, tests/test_gpu_tiler.py)."""
+    import torch
+    from paper_1611_02445_b200 import cli, workloads
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    assert workloads.generator_device() is None
+    assert workloads.generator_device(3) == 3
+    g = cli.parse_geometry("vessel:24:20:16")
+    assert g.shape == (24, 20, 16)
+    assert (g.types == 3).any() and (g.types == 4).any()
+    with pytest.raises(RuntimeError):
+        workloads.vessel_tree((16, 16, 16), device=0)
