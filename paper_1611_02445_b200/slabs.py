@@ -100,8 +100,11 @@ class SlabPlan:
             parts.append(types[:, :, lo:r.z0] if lo >= 0 else types[:, :, nz - TILE:nz])
         parts.append(types[:, :, r.z0:r.z1])
         if r.upper >= 0:
-            hi = r.z1 + TILE
-            parts.append(types[:, :, r.z1:hi] if hi <= nz else types[:, :, 0:TILE])
+            # the layer above; it wraps to z = 0..3 only across the periodic
+            # seam (r.z1 == nz).  A last layer of fewer than 4 nodes (nz % 4
+            # != 0, never periodic) is a partial ghost padded with SOLID.
+            parts.append(types[:, :, r.z1:min(r.z1 + TILE, nz)] if r.z1 < nz
+                         else types[:, :, 0:TILE])
         return np.ascontiguousarray(np.concatenate(parts, axis=2))
 
     def local_geometry(self, geometry, rank):
@@ -553,7 +556,10 @@ class DistributedSlabRunner:
         self.halo.wait(self.halo.start())
         self.slab.unpack(current=True)
 
-    def step(self, n=1):
+    def step(self, n=1, check=True):
+        """Advance n iterations.  ``check`` (default, like Solver.step): read
+        the status ring and the peer-wait error word at the end, raising
+        DivergenceError / RuntimeError (a neighbour that missed the step)."""
         sl = self.slab
         for _ in range(int(n)):
             if self.halo is None:
@@ -579,6 +585,14 @@ class DistributedSlabRunner:
             sl.unpack()
             sl.finish()
         sl.join()
+        if check:
+            self.check()
+
+    def check(self):
+        """Raise on divergence (status ring) or a peer-wait timeout."""
+        if self.ipc is not None:
+            self.ipc.check()
+        self.slab.solver.check()
 
     def barrier(self):
         if self.halo is not None:
@@ -615,7 +629,7 @@ class VirtualSlabs:
         for sl in self.slabs:
             sl.unpack(current=True)
 
-    def step(self, n=1):
+    def step(self, n=1, check=True):
         for _ in range(int(n)):
             if self.fused:
                 # each slab: interior on the main stream, boundary layers on
@@ -643,6 +657,9 @@ class VirtualSlabs:
                 sl.finish()
         for sl in self.slabs:
             sl.join()
+        if check:
+            for sl in self.slabs:
+                sl.solver.check()
 
     @staticmethod
     def _disarm(sl):

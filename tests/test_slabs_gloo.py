@@ -27,7 +27,10 @@ def _free_port():
 def _geometries():
     pack = geometry.generate_sphere_pack(16, 5, 0.7, seed=4, inlet_velocity=(0, 0, 0.02))
     chan = geometry.generate_channel("square", 10, axis=2, length=24, ends="periodic")
-    return {"pack": pack, "chan": chan}
+    # nz % 4 != 0 and one rank per tile layer: the last rank owns a partial
+    # layer of 2 nodes, which is the upper ghost of the rank below
+    cav = geometry.generate_cavity3d(10)
+    return {"pack": pack, "chan": chan, "cav": cav}
 
 
 def _initial(geo, dt=np.float64):
@@ -52,11 +55,16 @@ def _worker(rank, world, port, name, steps, out):
     if r.lower >= 0:
         idx += [(z % nz) for z in range(r.z0 - TILE, r.z0)]
     idx += list(range(r.z0, r.z1))
+    n_hi = 0
     if r.upper >= 0:
-        idx += [(z % nz) for z in range(r.z1, r.z1 + TILE)]
+        n_hi = min(TILE, nz - r.z1) if r.z1 < nz else TILE
+        idx += [(z % nz) for z in range(r.z1, r.z1 + n_hi)]
+    assert lgeo.shape[2] == len(idx)
+    assert np.array_equal(lgeo.types, geo.types[:, :, idx])
     f = np.ascontiguousarray(f0[:, :, :, idx])
     lo = TILE if r.lower >= 0 else 0
-    hi = f.shape[3] - (TILE if r.upper >= 0 else 0)
+    hi = f.shape[3] - n_hi
+    n_own_lo = min(TILE, r.z1 - r.z0)             # what the lower rank's upper ghost holds
     for _ in range(steps):
         o = c_oracle.DenseOracle(lgeo.types, "incompressible", 0.6, geo.inlet_velocity,
                                  geo.outlet_density, periodic=lgeo.periodic, f0=f, nthreads=1)
@@ -69,13 +77,13 @@ def _worker(rank, world, port, name, steps, out):
             ops.append(dist.P2POp(dist.isend, torch.from_numpy(f[..., hi - TILE:hi].copy()),
                                   r.upper))
         if r.lower >= 0:
-            ops.append(dist.P2POp(dist.isend, torch.from_numpy(f[..., lo:lo + TILE].copy()),
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(f[..., lo:lo + n_own_lo].copy()),
                                   r.lower))
         if r.lower >= 0:
             recv_lo = torch.empty(f[..., :TILE].shape, dtype=torch.float64)
             ops.append(dist.P2POp(dist.irecv, recv_lo, r.lower))
         if r.upper >= 0:
-            recv_hi = torch.empty(f[..., :TILE].shape, dtype=torch.float64)
+            recv_hi = torch.empty(f[..., :n_hi].shape, dtype=torch.float64)
             ops.append(dist.P2POp(dist.irecv, recv_hi, r.upper))
         for q in dist.batch_isend_irecv(ops):
             q.wait()
@@ -88,7 +96,8 @@ def _worker(rank, world, port, name, steps, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,world", [("pack", 2), ("chan", 2), ("chan", 3), ("pack", 3)])
+@pytest.mark.parametrize("name,world", [("pack", 2), ("chan", 2), ("chan", 3), ("pack", 3),
+                                        ("cav", 3)])
 def test_gloo_slab_decomposition_matches_single_domain(name, world):
     from oracle import c_oracle
     c_oracle.build()
@@ -132,6 +141,21 @@ def test_plan_balances_fluid_nodes():
     plan = SlabPlan(per, 4)
     assert plan.ranges[0].lower == 3 and plan.ranges[3].upper == 0
     assert plan.local_types(per.types, 0).shape[2] == 8 + 2 * TILE
+
+
+def test_plan_partial_last_layer_ghost():
+    """nz % 4 != 0 with the last rank owning only the partial top layer: the
+    rank below gets z = z1..nz-1 as its upper ghost, never the wrapped z = 0
+    wall (slabs.py local_types)."""
+    for n, world in ((10, 3), (30, 8)):
+        g = geometry.generate_cavity3d(n)
+        plan = SlabPlan(g, world)
+        assert plan.ranges[-1].z1 == n and not plan.periodic_z
+        for rk, r in enumerate(plan.ranges):
+            lt = plan.local_types(g.types, rk)
+            lo = r.z0 - TILE if r.lower >= 0 else r.z0
+            hi = min(r.z1 + TILE, n) if r.upper >= 0 else r.z1
+            assert np.array_equal(lt, g.types[:, :, lo:hi])
 
 
 def test_plan_run_matches_decomposition():
