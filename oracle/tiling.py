@@ -121,3 +121,42 @@ def from_blocks(blocks, table):
     """(t_n, 19, 64) stored blocks -> (19, t_n, 64) canonical (layout.py:161-167)."""
     perms = table_permutations(table)
     return np.stack([blocks[:, q, perms[q]] for q in range(19)])
+
+
+def meta_words(types, non_empty, periodic=(False,) * 3, a=4):
+    """(t_n, 64) u32 per-slot node words the device tiler must produce,
+    restated from the step contract:
+      bit 0       slot is a non-solid node inside the domain (R1)
+      bit q 1..18 the pull source n - e_q is inside the domain (wrapped on a
+                  periodic axis) and non-solid, i.e. g_q is a neighbour value
+                  and not the halfway bounce-back fill (R2)
+      bits 19-21  the node tag (geometry.py:17-24)
+      bits 22-24  the Zou-He face 2*axis + (0 low | 1 high) of an inlet /
+                  outlet node (classify_boundary_faces, boundaries.py:95-129)
+    """
+    from .dense import face_ids
+    from .numerics import E
+    nx, ny, nz = types.shape
+    dims = np.array([nx, ny, nz])
+    x = non_empty[:, 0:1].astype(np.int64) + SX
+    y = non_empty[:, 1:2].astype(np.int64) + SY
+    z = non_empty[:, 2:3].astype(np.int64) + SZ
+    inside = (x < nx) & (y < ny) & (z < nz)
+    xc, yc, zc = np.minimum(x, nx - 1), np.minimum(y, ny - 1), np.minimum(z, nz - 1)
+    tag = np.where(inside, types[xc, yc, zc], 0).astype(np.uint32)
+    w = np.where(tag != 0, 1 | (tag << 19), 0).astype(np.uint32)
+    for q in range(1, 19):
+        s = [x - E[q][0], y - E[q][1], z - E[q][2]]
+        ok = np.ones(x.shape, dtype=bool)
+        for ax in range(3):
+            if periodic[ax]:
+                s[ax] = s[ax] % dims[ax]
+            ok &= (s[ax] >= 0) & (s[ax] < dims[ax])
+        sx, sy, sz = (np.clip(s[ax], 0, dims[ax] - 1) for ax in range(3))
+        link = ok & (types[sx, sy, sz] != 0) & (tag != 0)
+        w |= np.where(link, np.uint32(1 << q), np.uint32(0))
+    f = face_ids(types, periodic)
+    face = np.where(inside, f[xc, yc, zc], -1)
+    io = (tag == 3) | (tag == 4)
+    w |= np.where(io, face.astype(np.int64) << 22, 0).astype(np.uint32)
+    return w
