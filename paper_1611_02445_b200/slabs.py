@@ -693,22 +693,43 @@ class VirtualSlabs:
         return torch.cat([sl.fields_owned() for sl in self.slabs], dim=1)
 
 
-class SlabChannel(DistributedSlabRunner):
-    """Bench workload for N ranks: the 256^2 channel periodic along z,
-    256 * N long, one 256^3 slab per rank (weak scaling)."""
+class SlabWorkload(DistributedSlabRunner):
+    """One rank of a bench run on any geometry: the slab of ``geometry``
+    this rank owns, started from the perturbed equilibrium of
+    workloads.perturbed_fields (seeded per rank) with its ghosts filled."""
 
-    def __init__(self, n, world, rank, precision="f64", table="b200", device=None,
-                 transport="nccl", arithmetic="reference"):
+    def __init__(self, geometry, world, rank, precision="f64", table="b200", device=None,
+                 transport="nccl", arithmetic="reference", u0=(0.0, 0.0, 0.02),
+                 storage="blocks", u_max_guard=0.05):
         from . import workloads
-        geo = workloads.channel_z(n, n * world)
+        if storage != "blocks":
+            table = None
         cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table,
-                               arithmetic=arithmetic)
-        super().__init__(geo, world, rank, cfg, device, transport)
+                               arithmetic=arithmetic, storage=storage, u_max_guard=u_max_guard)
+        super().__init__(geometry, world, rank, cfg, device, transport)
         s = self.slab.solver
-        rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.04),
+        rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, u0,
                                             seed=1234 + rank)
         s.init_from_macroscopic(rho, u)
         self.exchange_current()
+
+    def halo_bytes_per_step(self):
+        """Bytes this rank sends per step (80 values per boundary tile and
+        direction of travel); it receives as many."""
+        sl = self.slab
+        n = sum(b.numel() for b in (sl.send_up, sl.send_down) if b is not None)
+        return n * sl.solver.store.flat.element_size()
+
+
+class SlabChannel(SlabWorkload):
+    """The config-2 channel for N ranks: n^2 cross-section periodic along z,
+    n * N long, one n^3 slab per rank (weak scaling)."""
+
+    def __init__(self, n, world, rank, precision="f64", table="b200", device=None,
+                 transport="nccl", arithmetic="reference", u0=(0.0, 0.0, 0.02)):
+        from . import workloads
+        super().__init__(workloads.channel_z(n, n * world), world, rank, precision, table,
+                         device, transport, arithmetic, u0)
 
 
 def plan_run(geometry, world, precision="f64", storage="blocks", budget_gb=179.0):

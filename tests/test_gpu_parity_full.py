@@ -149,7 +149,7 @@ def test_step_channel_256(c_oracle, prec, arith):
     """BASELINE config 2, the bench workload: 256^3 channel periodic in z,
     perturbed equilibrium start (workloads.perturbed_fields), 10 steps."""
     geo = workloads.channel_z(256)
-    s = workloads.make_solver(geo, prec, u0=(0.0, 0.0, 0.04), arithmetic=arith)
+    s = workloads.make_solver(geo, prec, u0=(0.0, 0.0, 0.02), arithmetic=arith)
     r = _step_parity(c_oracle, s, geo, exact=arith == "reference")
     print(f"channel256 {prec} {arith}: rel f/rho/u = {r}")
 

@@ -110,10 +110,17 @@ def test_acceptance4_channel_tiling_sweep():
                                     Fraction(15, 16)}
 
 
-@pytest.mark.parametrize("transport", ["ipc", "gloo"])
-def test_bench_two_ranks_on_one_gpu(transport):
+@pytest.mark.parametrize("transport,workload", [
+    ("ipc", ["--scale-edge", "64", "--scale-length", "16"]),
+    ("gloo", ["--scale-edge", "64", "--scale-length", "16"]),
+    ("ipc", ["--workload", "channel", "--edge", "64"]),
+    ("ipc", ["--workload", "vessel_strong", "--vessel-shape", "64,64,128"])])
+def test_bench_two_ranks_on_one_gpu(transport, workload):
     """The N > 1 bench path (torchrun, fused IPC halo or host-staged gloo
-    halo) runs end to end with both ranks on cuda:0 and prints one line."""
+    halo) runs end to end with both ranks on cuda:0 and prints one line:
+    the default dense weak-scaling workload of BASELINE config 5 at a
+    reduced edge (64 x 64 x 16 per rank instead of 1024 x 1024 x 128), the
+    config-2 channel and the strong-scaling vessel tree."""
     import json
     import os
     import socket
@@ -126,7 +133,7 @@ def test_bench_two_ranks_on_one_gpu(transport):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
                         "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
                         "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "6",
-                        "--warmup", "3", "--edge", "64", "--transport", transport],
+                        "--warmup", "3", "--transport", transport] + workload,
                        cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
@@ -135,3 +142,11 @@ def test_bench_two_ranks_on_one_gpu(transport):
     assert line["n_gpus"] == 2 and line["config"]["halo"] == transport
     assert line["config"]["shared_gpu_test_mode"] is True and line["value"] > 0
     assert line["e2e"]["value"] > 0
+    cfg = line["config"]
+    assert len(cfg["memory_gb_per_rank"]) == 2 and len(cfg["halo_bytes_sent_per_step_per_rank"]) == 2
+    assert all(b > 0 for b in cfg["halo_bytes_sent_per_step_per_rank"])
+    if "--scale-edge" in workload:
+        assert cfg["workload"] == "dense64x64x16_per_gpu_weak_f64" and line["scaling"] == "weak"
+        assert cfg["n_fn_total"] == 2 * 64 * 64 * 16
+    if "vessel_strong" in workload:
+        assert line["scaling"] == "strong"
