@@ -15,6 +15,10 @@ Everything here calls the reference package ``tilelbm`` (imported from
 * tiling.npz    -- build_tiling (tiling.py:51-83), _neighbor_indices over the
                    27 deltas and _tile_nonsolid_blocks (txmodel.py:145-173) of
                    reference-generated geometries (cavity, channels, packs).
+* faces.npz     -- classify_boundary_faces (boundaries.py:95-129) on
+                   reference-generated geometries with inlet/outlet on the
+                   x, y and z faces and a box with both kinds on all six
+                   faces; tile_utilization (tiling.py:120-140) statistics.
 * step.npz      -- the step has no reference implementation, so
                    it is composed here from reference functions only
                    (classify_boundary_faces, FACE_CLOSURES, zou_he_*,
@@ -174,9 +178,80 @@ def step():
     np.savez_compressed(os.path.join(HERE, "step.npz"), **out)
 
 
+def six_face_box():
+    """Interior FLUID box whose six faces carry inlets (low faces) and
+    outlets (high faces) inside a bounce-back rim, plus a few interior
+    solids and walls."""
+    t = np.ones((12, 10, 9), dtype=np.uint8)
+    for a in range(3):
+        lo = [slice(None)] * 3
+        hi = [slice(None)] * 3
+        lo[a], hi[a] = 0, -1
+        t[tuple(lo)] = rg.NodeType.VELOCITY_INLET
+        t[tuple(hi)] = rg.NodeType.PRESSURE_OUTLET
+    # edges and corners (on two or three faces) -> bounce-back rim
+    x, y, z = np.meshgrid(*(np.arange(n) for n in t.shape), indexing="ij")
+    on = sum(((c == 0) | (c == n - 1)).astype(int) for c, n in zip((x, y, z), t.shape))
+    t[on >= 2] = rg.NodeType.BB_WALL
+    t[5, 4, 4] = rg.NodeType.SOLID
+    t[6, 5, 3] = rg.NodeType.BB_WALL
+    t[0, 3, 3] = rg.NodeType.SOLID           # a hole in the x-low inlet plane
+    t[11, 4, 6] = rg.NodeType.BB_WALL        # a wall node in the x-high outlet plane
+    return rg.Geometry(t, inlet_velocity=(0.01, 0.0, 0.0), outlet_density=1.0)
+
+
+def face_cases():
+    return {
+        "cavity10": rg.generate_cavity3d(10),
+        "chan_io_z": rg.generate_channel("circle", 10, axis=2, offsets=(3, 1), length=9,
+                                         ends="io"),
+        "chan_io_x": rg.generate_channel("square", 8, axis=0, offsets=(1, 1), length=13,
+                                         ends="io", inlet_velocity=(0.02, 0.0, 0.0)),
+        "chan_io_y": rg.generate_channel("circle", 9, axis=1, offsets=(2, 1), length=7,
+                                         ends="io", inlet_velocity=(0.0, 0.02, 0.0)),
+        "pack_z": rg.generate_sphere_pack(22, 8, 0.55, seed=7),
+        "pack_x": rg.generate_sphere_pack(17, 6, 0.7, seed=3, flow_axis=0),
+        "pack_y": rg.generate_sphere_pack(19, 6, 0.6, seed=5, flow_axis=1),
+        "box6": six_face_box(),
+    }
+
+
+def faces():
+    out = {}
+    for name, g in face_cases().items():
+        out[f"{name}_types"] = g.types
+        res = rb.classify_boundary_faces(g)
+        out[f"{name}_keys"] = np.array(sorted(res), dtype=np.int64).reshape(-1, 2)
+        for (axis, sign), (inlet, outlet) in res.items():
+            out[f"{name}_{axis}_{sign}_in"] = inlet
+            out[f"{name}_{axis}_{sign}_out"] = outlet
+        st = rt.tile_utilization(rt.build_tiling(g), g)
+        out[f"{name}_util"] = np.array([st.t_n, st.n_fn, st.eta_t, st.n_tfn, st.n_tsn,
+                                        st.eta_f, st.eta_e], dtype=np.float64)
+    # rejected: an inlet on a corner (three faces) and an outlet inside
+    bad = np.ones((6, 6, 6), dtype=np.uint8)
+    bad[0, 0, 0] = rg.NodeType.VELOCITY_INLET
+    out["bad_corner_types"] = bad
+    bad = np.ones((6, 6, 6), dtype=np.uint8)
+    bad[2, 3, 3] = rg.NodeType.PRESSURE_OUTLET
+    out["bad_interior_types"] = bad
+    for k in ("bad_corner", "bad_interior"):
+        try:
+            rb.classify_boundary_faces(rg.Geometry(out[f"{k}_types"]))
+            raise AssertionError("reference accepted a misplaced inlet/outlet")
+        except ValueError as exc:
+            out[f"{k}_msg"] = np.array(str(exc))
+    np.savez_compressed(os.path.join(HERE, "faces.npz"), **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:                      # regenerate selected files only
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     lattice()
     numerics()
     tiling()
+    faces()
     step()
     print("golden vectors written to", HERE)

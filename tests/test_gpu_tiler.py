@@ -87,15 +87,65 @@ def test_sphere_pack_counts():
     assert st.n_fn == g.nonsolid_count()
 
 
-def test_utilization_matches_reference(reference, golden):
-    rt, rg = reference.tiling, reference.geometry
-    for b in (10, 13):
-        a = rg.generate_cavity3d(b)
-        ref = rt.tile_utilization(rt.build_tiling(a), a)
-        g = geo_mod.generate_cavity3d(b)
-        got = tiling.tile_utilization(tiling.build_tiling(g), g)
-        assert (got.t_n, got.n_fn, got.eta_t, got.eta_f, got.eta_e) == \
-            (ref.t_n, ref.n_fn, ref.eta_t, ref.eta_f, ref.eta_e)
+FACE_CASES = ("cavity10", "chan_io_z", "chan_io_x", "chan_io_y", "pack_z", "pack_x", "pack_y",
+              "box6")
+
+
+@pytest.mark.parametrize("name", FACE_CASES)
+def test_utilization_golden(golden, name):
+    """tile_utilization (tiling.py:120-140) == the reference's statistics
+    (tests/golden/faces.npz, made by the reference), exactly."""
+    gd = golden("faces")
+    g = geo_mod.Geometry(gd[f"{name}_types"])
+    st = tiling.tile_utilization(tiling.build_tiling(g), g)
+    want = gd[f"{name}_util"]
+    assert (st.t_n, st.n_fn) == (int(want[0]), int(want[1]))
+    assert np.array_equal(np.array([st.eta_t, st.n_tfn, st.n_tsn, st.eta_f, st.eta_e]),
+                          want[2:])
+
+
+@pytest.mark.parametrize("name", FACE_CASES)
+def test_classify_boundary_faces_golden(golden, name):
+    """boundaries.classify_boundary_faces (boundaries.py:95-129) == the
+    reference's output: same keys, same flat C-order inlet / outlet ids,
+    on x, y and z faces and all six faces of one box; and the device node
+    words carry the same face code for every inlet / outlet slot."""
+    from paper_1611_02445_b200 import boundaries
+    gd = golden("faces")
+    types = gd[f"{name}_types"]
+    g = geo_mod.Geometry(types)
+    got = boundaries.classify_boundary_faces(g)
+    keys = [(int(a), int(s)) for a, s in gd[f"{name}_keys"]]
+    assert sorted(got) == sorted(keys)
+    face = np.full(types.size, -1, dtype=np.int64)
+    for a, s in keys:
+        inl, outl = got[(a, s)]
+        assert np.array_equal(inl, gd[f"{name}_{a}_{s}_in"])
+        assert np.array_equal(outl, gd[f"{name}_{a}_{s}_out"])
+        assert boundaries.FACE_CLOSURES[(a, s)].face_id == 2 * a + (0 if s > 0 else 1)
+        face[inl] = face[outl] = 2 * a + (0 if s > 0 else 1)
+    grid = tiling.build_tiling(g)
+    meta = grid.device.meta.cpu().numpy().astype(np.int64)
+    ne = grid.non_empty
+    j = np.arange(64)
+    x, y, z = ne[:, 0:1] + (j & 3), ne[:, 1:2] + ((j >> 2) & 3), ne[:, 2:3] + (j >> 4)
+    nx, ny, nz = types.shape
+    inside = (x < nx) & (y < ny) & (z < nz)
+    flat = (np.minimum(x, nx - 1) * ny + np.minimum(y, ny - 1)) * nz + np.minimum(z, nz - 1)
+    io = inside & (face[flat] >= 0)
+    assert np.array_equal((meta[io] >> 22) & 7, face[flat][io])
+
+
+@pytest.mark.parametrize("k", ["bad_corner", "bad_interior"])
+def test_classify_boundary_faces_rejects_like_reference(golden, k):
+    from paper_1611_02445_b200 import boundaries
+    gd = golden("faces")
+    g = geo_mod.Geometry(gd[f"{k}_types"])
+    with pytest.raises(ValueError) as exc:
+        boundaries.classify_boundary_faces(g)
+    assert str(exc.value) == str(gd[f"{k}_msg"])
+    with pytest.raises(ValueError):
+        tiling.build_tiling(g)
 
 
 def test_rejects_bad_faces():

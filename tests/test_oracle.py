@@ -92,6 +92,57 @@ def test_tiling_golden(golden):
         assert np.array_equal(ot.nonsolid_blocks(types, ne), g[f"{name}_nonsolid"]), name
 
 
+def _golden_faces(gd, name):
+    """{(axis, sign): (inlet ids, outlet ids)} of one faces.npz case."""
+    return {(int(a), int(s)): (gd[f"{name}_{a}_{s}_in"], gd[f"{name}_{a}_{s}_out"])
+            for a, s in gd[f"{name}_keys"]}
+
+
+FACE_CASES = ("cavity10", "chan_io_z", "chan_io_x", "chan_io_y", "pack_z", "pack_x", "pack_y",
+              "box6")
+
+
+def test_face_ids_golden(golden):
+    """oracle.dense.face_ids (the per-node face code the oracle step and the
+    device node words use) == classify_boundary_faces of the reference
+    (boundaries.py:95-129) on x-, y- and z-face inlets/outlets and a box
+    with both kinds on all six faces; misplaced nodes raise the same error."""
+    gd = golden("faces")
+    seen = set()
+    for name in FACE_CASES:
+        types = gd[f"{name}_types"]
+        f = dense.face_ids(types).ravel()
+        want = np.full(types.size, -1, dtype=np.int64)
+        for (axis, sign), (inl, outl) in _golden_faces(gd, name).items():
+            code = 2 * axis + (0 if sign > 0 else 1)
+            want[inl] = code
+            want[outl] = code
+            seen.add(code)
+            assert np.all(types.ravel()[inl] == 3) and np.all(types.ravel()[outl] == 4)
+        assert np.array_equal(f, want), name
+    assert seen == set(range(6))
+    for k in ("bad_corner", "bad_interior"):
+        with pytest.raises(ValueError) as exc:
+            dense.face_ids(gd[f"{k}_types"])
+        assert str(exc.value) == str(gd[f"{k}_msg"])
+
+
+def test_face_golden_matches_live_reference(reference, golden):
+    """The committed faces.npz is what the reference computes today."""
+    gd = golden("faces")
+    rb, rg, rt = reference.boundaries, reference.geometry, reference.tiling
+    for name in FACE_CASES:
+        g = rg.Geometry(gd[f"{name}_types"])
+        got = rb.classify_boundary_faces(g)
+        want = _golden_faces(gd, name)
+        assert sorted(got) == sorted(want)
+        for k in want:
+            assert all(np.array_equal(a, b) for a, b in zip(got[k], want[k]))
+        st = rt.tile_utilization(rt.build_tiling(g), g)
+        assert np.array_equal(np.array([st.t_n, st.n_fn, st.eta_t, st.n_tfn, st.n_tsn,
+                                        st.eta_f, st.eta_e]), gd[f"{name}_util"])
+
+
 def test_face_closures_match_reference(reference):
     rb = reference.boundaries
     for key, c in rb.FACE_CLOSURES.items():
