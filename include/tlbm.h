@@ -131,6 +131,18 @@ int tlbm_collide_lbgk(void *d_f, int dtype, int fluid, int64_t n, double tau,
  * float64 19x19 operator h_op (collision.py:234-247). */
 int tlbm_collide_mrt(void *d_f, int dtype, int fluid, int64_t n, const double *h_op,
                      uint32_t *d_flags, void *stream);
+/* collide_mrt with an explicit float64 operator on float32 populations
+ * (collision.py:234-247 under NumPy's promotion): f + apply_operator(op,
+ * feq - f) with the wide accumulation of tlbm_apply_operator. */
+int tlbm_collide_mrt_wide(void *d_f, int fluid, int64_t n, const double *h_op,
+                          uint32_t *d_flags, void *stream);
+/* apply_operator (collision.py:216-231) on (19, n) canonical data:
+ * out[i] = sum over j with op[i][j] != 0, in j order, of op[i][j] * delta[j],
+ * in the data dtype.  wide = 1 with float32 data: a float64 operator, each
+ * term and partial sum formed in float64 and rounded to float32 after every
+ * accumulation (NumPy's `acc += c * delta[j]` for a float64 scalar c). */
+int tlbm_apply_operator(const void *d_delta, void *d_out, int dtype, int64_t n,
+                        const double *h_op, int wide, void *stream);
 /* Zou-He closure in place on (19, m) canonical populations of nodes on one
  * face (face = 2*axis + (0 low | 1 high)); kind 0 = velocity inlet with
  * (ux,uy,uz) (boundaries.py:139-157), 1 = pressure outlet with rho0

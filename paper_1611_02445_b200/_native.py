@@ -69,6 +69,8 @@ _PROTOS = {
     "tlbm_equilibrium": (c_int, [c_vp, c_vp, c_int, c_int, c_i64, c_vp, c_vp]),
     "tlbm_collide_lbgk": (c_int, [c_vp, c_int, c_int, c_i64, c_dbl, c_vp, c_vp]),
     "tlbm_collide_mrt": (c_int, [c_vp, c_int, c_int, c_i64, c_vp, c_vp, c_vp]),
+    "tlbm_collide_mrt_wide": (c_int, [c_vp, c_int, c_i64, c_vp, c_vp, c_vp]),
+    "tlbm_apply_operator": (c_int, [c_vp, c_vp, c_int, c_i64, c_vp, c_int, c_vp]),
     "tlbm_zou_he": (c_int, [c_vp, c_int, c_int, c_int, c_int, c_i64, c_dbl, c_dbl,
                             c_dbl, c_dbl, c_vp, c_vp]),
     "tlbm_halo": (c_int, [c_vp, c_int, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp]),

@@ -196,45 +196,52 @@ def mrt_operator(rates, dtype=np.float64):
 def apply_operator(op, delta):
     """A 19x19 operator applied to (19, ...) data as 19 fixed-order row
     accumulations that skip exact-zero coefficients (collision.py:216-231),
-    on the GPU.  Each term is computed as numpy computes ``acc += c *
-    delta[j]`` with ``c`` an element of ``op``: in the promoted type of
-    (op, delta), then stored in delta's dtype -- bit-identical to the
-    reference for float32 and float64 data."""
+    in one kernel (tlbm_apply_operator).  Each term is computed as numpy
+    computes ``acc += c * delta[j]`` with ``c`` an element of ``op``: in the
+    promoted type of (op, delta), then stored in delta's dtype -- bit-
+    identical to the reference for float32 and float64 data."""
     opa = np.asarray(op)
     if opa.shape != (Q, Q):
         raise ValueError(f"operator must be 19x19, got {opa.shape}")
     dt, as_np = _to_device(delta)
     if dt.shape[0] != Q:
         raise ValueError(f"expected (19, ...) data, got {tuple(dt.shape)}")
-    wide = torch.float64 if (opa.dtype == np.float64 or dt.dtype == torch.float64) \
-        else torch.float32
-    out = torch.empty_like(dt)
-    dw = dt.to(wide)
-    for i in range(Q):
-        acc = torch.zeros_like(dt[0])
-        for j in range(Q):
-            c = opa[i, j]
-            if c != 0.0:
-                acc = (acc.to(wide) + float(c) * dw[j]).to(dt.dtype)
-        out[i] = acc
+    wide = int(opa.dtype == np.float64 and dt.dtype == torch.float32)
+    op64 = np.ascontiguousarray(opa, dtype=np.float64)
+    src = dt.contiguous()
+    out = torch.empty_like(src)
+    n = src.numel() // Q
+    nat.call("tlbm_apply_operator", nat.ptr(src), nat.ptr(out), nat.code_of(src.dtype), n,
+             op64.ctypes.data, wide, nat.stream_ptr(src.device))
     return _back(out, as_np)
 
 
 def collide_mrt(model, f, rates=None, operator=None):
-    """f + M^-1 S M (feq - f) (collision.py:234-247) on the GPU."""
+    """f + M^-1 S M (feq - f) (collision.py:234-247) on the GPU.  With
+    ``rates`` the operator is built in float64 and rounded to f's dtype, as
+    the reference does; an explicit float64 ``operator`` on float32 data is
+    applied the way NumPy promotes it (each term in float64, rounded into
+    the float32 accumulator)."""
+    ft, as_np = _to_device(f)
     if operator is None:
         if rates is None:
             raise ValueError("either moment rates or a precomputed operator is required")
         operator = mrt_operator(rates, dtype=np.float64)
+        wide = False
+    else:
+        wide = np.asarray(operator).dtype == np.float64 and ft.dtype == torch.float32
     op = np.ascontiguousarray(np.asarray(operator, dtype=np.float64))
-    ft, as_np = _to_device(f)
     out = ft.clone()
     rest = tuple(ft.shape[1:])
     n = int(np.prod(rest)) if rest else 1
     flags = _flags(ft.device)
     code = fluid_code(model)
-    nat.call("tlbm_collide_mrt", nat.ptr(out), nat.code_of(ft.dtype), code, n,
-             op.ctypes.data, nat.ptr(flags), nat.stream_ptr(ft.device))
+    if wide:
+        nat.call("tlbm_collide_mrt_wide", nat.ptr(out), code, n, op.ctypes.data, nat.ptr(flags),
+                 nat.stream_ptr(ft.device))
+    else:
+        nat.call("tlbm_collide_mrt", nat.ptr(out), nat.code_of(ft.dtype), code, n,
+                 op.ctypes.data, nat.ptr(flags), nat.stream_ptr(ft.device))
     if code == nat.QUASI:
         _raise_if_diverged(flags, "quasi-compressible flow")
     return _back(out, as_np)

@@ -143,6 +143,57 @@ __global__ void collide_mrt_kernel(T *f, long long n, const OpParam<T> op, uint3
     if (flags && st) atomicOr(flags, st);
 }
 
+// apply_operator (collision.py:216-231): out[i] = sum over j with op[i][j]
+// != 0, in j order, of op[i][j] * delta[j].  WIDE (float32 data, float64
+// operator): NumPy evaluates `acc += c * delta[j]` with a float64 scalar c
+// in float64 and rounds into the float32 accumulator (NEP 50), so each term
+// and partial sum is formed in double and rounded to T after every add.
+template <class T, int WIDE>
+__device__ __forceinline__ void apply_op_column(const double *op, const T (&d)[Q], T (&out)[Q]) {
+#pragma unroll
+    for (int i = 0; i < Q; ++i) {
+        T acc = T(0);
+        for (int j = 0; j < Q; ++j) {
+            const double c = op[i * Q + j];
+            if (c == 0.0) continue;
+            if (WIDE) acc = T(double(acc) + c * double(d[j]));
+            else acc = acc + T(c) * d[j];
+        }
+        out[i] = acc;
+    }
+}
+
+template <class T, int WIDE>
+__global__ void apply_operator_kernel(const T *delta, T *out, long long n,
+                                      const OpParam<double> op) {
+    for (long long i = gtid(); i < n; i += gstride()) {
+        T d[Q], r[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) d[q] = delta[q * n + i];
+        apply_op_column<T, WIDE>(op.op, d, r);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) out[q * n + i] = r[q];
+    }
+}
+
+// collide_mrt (collision.py:234-247) with a float64 operator on float32
+// populations: f + apply_operator(op, feq - f) with the wide accumulation
+template <int QUASI>
+__global__ void collide_mrt_wide_kernel(float *f, long long n, const OpParam<double> op,
+                                        uint32_t *flags) {
+    uint32_t st = 0;
+    for (long long i = gtid(); i < n; i += gstride()) {
+        float g[Q], d[Q], r[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) g[q] = f[q * n + i];
+        st |= mrt_deviations<float, QUASI>(g, d, float(HUGE_VAL));
+        apply_op_column<float, 1>(op.op, d, r);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) f[q * n + i] = g[q] + r[q];
+    }
+    if (flags && st) atomicOr(flags, st);
+}
+
 template <class T, int QUASI>
 __global__ void collide_kernel(T *f, long long n, double inv_tau, uint32_t *flags) {
     uint32_t st = 0;
@@ -295,6 +346,44 @@ extern "C" int tlbm_collide_mrt(void *d_f, int dtype, int fluid, int64_t n, cons
         collide_mrt_kernel<T, QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
             static_cast<T *>(d_f), n, op, d_flags);
         return launch_check("collide_mrt_kernel");
+    });
+}
+
+extern "C" int tlbm_apply_operator(const void *d_delta, void *d_out, int dtype, int64_t n,
+                                   const double *h_op, int wide, void *stream) {
+    if (!h_op || !d_delta || !d_out) {
+        set_error("tlbm_apply_operator: operator, input and output required");
+        return TLBM_ERR_ARG;
+    }
+    if (n == 0) return TLBM_OK;
+    OpParam<double> op;
+    for (int k = 0; k < Q * Q; ++k) op.op[k] = h_op[k];
+    return dispatch(dtype, 0, 0, [&]<class T, int QU, int TB>() {
+        auto *in = static_cast<const T *>(d_delta);
+        auto *out = static_cast<T *>(d_out);
+        if (wide && sizeof(T) == 4)
+            apply_operator_kernel<T, 1><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+                in, out, n, op);
+        else
+            apply_operator_kernel<T, 0><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+                in, out, n, op);
+        return launch_check("apply_operator_kernel");
+    });
+}
+
+extern "C" int tlbm_collide_mrt_wide(void *d_f, int fluid, int64_t n, const double *h_op,
+                                     uint32_t *d_flags, void *stream) {
+    if (!h_op) {
+        set_error("tlbm_collide_mrt_wide: operator required");
+        return TLBM_ERR_ARG;
+    }
+    if (n == 0) return TLBM_OK;
+    OpParam<double> op;
+    for (int k = 0; k < Q * Q; ++k) op.op[k] = h_op[k];
+    return dispatch(TLBM_F32, fluid, 0, [&]<class T, int QU, int TB>() {
+        collide_mrt_wide_kernel<QU><<<grid_capped(n), 256, 0, as_stream(stream)>>>(
+            static_cast<float *>(d_f), n, op, d_flags);
+        return launch_check("collide_mrt_wide_kernel");
     });
 }
 

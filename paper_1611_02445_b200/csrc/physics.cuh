@@ -299,29 +299,14 @@ __device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, T guard_sq) {
     return status_of<T, QUASI>(rho, usq, guard_sq);
 }
 
-// MRT collide in place: g <- g + A (feq - g) with the velocity-space operator
-// A = M^-1 S M (collision.py:206-247), A row-major in op[19*19].  Rows are
-// accumulated from 0 in column order like apply_operator (collision.py:216-
-// 231).  The reference skips exact-zero coefficients; adding their c * d = 0
-// terms instead leaves every finite result bit-identical (x + 0 = x), so the
-// kernel runs the dense 19 x 19 product with coefficients read straight from
-// the kernel-parameter constant bank (compile-time offsets after unrolling).
-//
-// grouped (default operator, checked on the host per launch): op holds, per
-// column j, only the distinct values of A[.][j] (mrt_pattern.cuh), and each
-// distinct product c * d[j] is computed once and added to every row that
-// holds c -- the same rounded product in the same row order, so the result
-// equals the dense product bit for bit (up to the sign of an all-zero row
-// sum: the first term starts the row instead of 0 + term).  209 instead of
-// 361 multiplies, and 19 independent row chains.
+// feq - g in the reference's order (collision.py:94-121, 244-246): the
+// deviations the MRT operator is applied to; returns the status word
 template <class T, int QUASI>
-__device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq,
-                                                bool grouped = false) {
+__device__ __forceinline__ uint32_t mrt_deviations(const T (&g)[Q], T (&d)[Q], T guard_sq) {
     T rho, u[3];
     moments<T, QUASI>(g, rho, u);
     const T usq = speed_sq(u);
     const T c15 = T(1.5) * usq;
-    T d[Q];
     d[0] = feq_of<T, QUASI>(0, rho, (T(3.0) * T(0) + T(4.5) * T(0) * T(0)) - c15) - g[0];
 #pragma unroll
     for (int q = 1; q < Q; ++q) {
@@ -342,6 +327,29 @@ __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_
         d[q] = feq_of<T, QUASI>(q, rho, (A + B) - c15) - g[q];
         d[o] = feq_of<T, QUASI>(o, rho, (B - A) - c15) - g[o];
     }
+    return status_of<T, QUASI>(rho, usq, guard_sq);
+}
+
+// MRT collide in place: g <- g + A (feq - g) with the velocity-space operator
+// A = M^-1 S M (collision.py:206-247), A row-major in op[19*19].  Rows are
+// accumulated from 0 in column order like apply_operator (collision.py:216-
+// 231).  The reference skips exact-zero coefficients; adding their c * d = 0
+// terms instead leaves every finite result bit-identical (x + 0 = x), so the
+// kernel runs the dense 19 x 19 product with coefficients read straight from
+// the kernel-parameter constant bank (compile-time offsets after unrolling).
+//
+// grouped (default operator, checked on the host per launch): op holds, per
+// column j, only the distinct values of A[.][j] (mrt_pattern.cuh), and each
+// distinct product c * d[j] is computed once and added to every row that
+// holds c -- the same rounded product in the same row order, so the result
+// equals the dense product bit for bit (up to the sign of an all-zero row
+// sum: the first term starts the row instead of 0 + term).  209 instead of
+// 361 multiplies, and 19 independent row chains.
+template <class T, int QUASI>
+__device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq,
+                                                bool grouped = false) {
+    T d[Q];
+    const uint32_t st = mrt_deviations<T, QUASI>(g, d, guard_sq);
     if (TLBM_MRT_GROUPED && grouped) {
         T acc[Q];
 #pragma unroll
@@ -365,7 +373,7 @@ __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_
             g[i] = g[i] + acc;
         }
     }
-    return status_of<T, QUASI>(rho, usq, guard_sq);
+    return st;
 }
 
 // ---- Zou-He (boundaries.py:53-92 closures, 132-195 arithmetic) -----------

@@ -105,9 +105,32 @@ def test_collide_mrt_golden(golden, dn, mn):
     g = golden("numerics")
     f = g[f"f_{dn}"]
     op = golden("lattice")["mrt_op_0.6"]
-    out = collision.collide_mrt(MODELS[mn], f, operator=op)
-    assert out.dtype == f.dtype
-    assert np.array_equal(out, g[f"mrt_{dn}_{mn}"])
+    # the golden is collide_mrt(rates=...): operator built in float64 and
+    # rounded to f's dtype (collision.py:241-243)
+    for kw in ({"rates": collision.default_mrt_rates(0.6)}, {"operator": op.astype(f.dtype)}):
+        out = collision.collide_mrt(MODELS[mn], f, **kw)
+        assert out.dtype == f.dtype
+        assert np.array_equal(out, g[f"mrt_{dn}_{mn}"])
+
+
+@pytest.mark.parametrize("mn", MODELS)
+def test_collide_mrt_float64_operator_on_float32(golden, mn):
+    """An explicit float64 operator on float32 populations follows NumPy's
+    promotion: each c * delta term in float64, rounded into the
+    float32 accumulator -- the oracle's numpy restatement of collision.py:
+    216-247 on the same inputs, bit for bit."""
+    from oracle import numerics as onm
+    g = golden("numerics")
+    f = g["f_f32"]
+    op = golden("lattice")["mrt_op_0.6"]
+    assert op.dtype == np.float64
+    want = onm.collide_mrt(MODELS[mn].value, f, operator=op)
+    assert want.dtype == np.float32
+    got = collision.collide_mrt(MODELS[mn], f, operator=op)
+    assert got.dtype == np.float32 and np.array_equal(got, want)
+    # and it differs from the operator rounded to float32 first
+    narrow = collision.collide_mrt(MODELS[mn], f, operator=op.astype(np.float32))
+    assert not np.array_equal(narrow, want)
 
 
 def test_mrt_setup_matches_oracle(golden):
