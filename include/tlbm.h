@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define TLBM_ABI_VERSION 2
+#define TLBM_ABI_VERSION 3
 
 enum { TLBM_F64 = 0, TLBM_F32 = 1 };
 enum { TLBM_INCOMPRESSIBLE = 0, TLBM_QUASI = 1 };
@@ -215,6 +215,16 @@ typedef struct {
      * then point at the neighbour's copy, not at its ghost layer */
     const int64_t *halo_up_cbase;
     const int64_t *halo_down_cbase;
+    /* node-parallel traversal of a compact store (node_meta NULL = one
+     * 64-thread group per tile): one thread per non-solid node, nodes
+     * [node_begin, node_end) in store order (tile-major, rank-minor) --
+     * the nodes of tiles [tile_begin, tile_end) -- with the per-node records
+     * of tlbm_compact_nodes; needs 19 * n_fn < 2^32 (rel32). */
+    const uint32_t *node_meta;
+    const void *node_rec;
+    const int32_t *unit_tile;
+    const void *entries;
+    int64_t node_begin, node_end;
 } tlbm_step_args;
 
 int tlbm_step(const tlbm_step_args *a, void *stream);
@@ -222,6 +232,24 @@ int tlbm_step(const tlbm_step_args *a, void *stream);
 /* (t_n, 64) uint8: rank[t][j] = non-solid slots of tile t before slot j
  * (255 for a solid slot). */
 int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank, void *stream);
+/* Per-node records of a compact store for the node-parallel step
+ * (tlbm_step_args.node_meta; one thread per non-solid node, so a tile's
+ * solid slots cost no lanes).  Node n (store order: tile-major, rank-minor):
+ *   d_node_meta[n] = its node word (bits 0-24) | slot << 25
+ *   d_node_rec[n]  = 4 x uint32: the rank, in its source tile, of the value
+ *                    it pulls in direction q = 1..18 (6 bits each, five per
+ *                    word: q-1 = 5w + i at bits 6i of word w), its own rank
+ *                    at bits 18-23 and its tile - d_unit_tile[n / 64] at
+ *                    bits 24-29 of word 3
+ *   d_unit_tile[u] = the tile of node 64u            (ceil(n_fn / 64))
+ *   d_entries[t][k] = {low 32 bits of cbase, cnf} of neighbour entry k of
+ *                    tile t (the tile itself where there is none)  (t_n x 27)
+ * d_base / d_nf / d_rank: the compact store's cbase / cnf / crank. */
+int tlbm_compact_nodes(const uint32_t *d_meta, const int32_t *d_nbr, int64_t t_n,
+                       int64_t n_fn, const int64_t *d_base, const int32_t *d_nf,
+                       const uint8_t *d_rank, uint32_t *d_node_meta, uint32_t *d_node_rec,
+                       int32_t *d_unit_tile, uint32_t *d_entries, void *stream);
+
 /* Convert one copy between the paper's XYZ block store ((t_n, 19, 64)
  * blocks) and the compact store (19 * n_fn values); to_compact 1: blocks ->
  * compact, 0: compact -> blocks (solid slots written as the rest state w_q). */

@@ -12,7 +12,7 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TLBM_LIB") or os.path.join(HERE, "lib", "libtlbm.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 F64, F32 = 0, 1
 INCOMPRESSIBLE, QUASI = 0, 1
@@ -37,7 +37,9 @@ class StepArgs(ctypes.Structure):
                 ("collision", c_int), ("mrt_op", c_vp), ("arith", c_int),
                 ("iter_counter", c_vp), ("iter_add", c_i64), ("ring_len", c_int),
                 ("cbase", c_vp), ("cnf", c_vp), ("crank", c_vp), ("order", c_vp),
-                ("halo_up_cbase", c_vp), ("halo_down_cbase", c_vp)]
+                ("halo_up_cbase", c_vp), ("halo_down_cbase", c_vp),
+                ("node_meta", c_vp), ("node_rec", c_vp), ("unit_tile", c_vp),
+                ("entries", c_vp), ("node_begin", c_i64), ("node_end", c_i64)]
 
 
 _PROTOS = {
@@ -79,6 +81,8 @@ _PROTOS = {
     "tlbm_vessel_tree": (c_int, [c_vp, c_vp, c_int, c_int, c_int, c_int, c_int, c_vp, c_vp,
                                  c_vp]),
     "tlbm_compact_ranks": (c_int, [c_vp, c_i64, c_vp, c_vp]),
+    "tlbm_compact_nodes": (c_int, [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                   c_vp, c_vp, c_vp]),
     "tlbm_sphere_cover": (c_int, [c_vp, c_i64, c_i64, c_int, c_dbl, c_vp, c_vp]),
     "tlbm_halo_compact": (c_int, [c_vp, c_int, c_i64, c_i64, c_int, c_int, c_vp, c_vp, c_vp,
                                   c_vp, c_vp]),

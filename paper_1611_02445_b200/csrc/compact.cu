@@ -124,6 +124,101 @@ extern "C" int tlbm_compact_convert(const void *d_in, void *d_out, int dtype, in
                                                  to_compact, s);
 }
 
+// ---- per-node records for the node-parallel step ---------------------------
+// (layout in include/tlbm.h: tlbm_compact_nodes; kernel step_kernel_nodes)
+namespace tlbm {
+namespace {
+
+// the tile of node 64u, for every unit u that starts inside tile t
+__global__ void unit_tile_kernel(const long long *base, const int *nf, long long t_n,
+                                 int *unit_tile) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < t_n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long n0 = base[t] / Q, n1 = n0 + nf[t];
+        for (long long n = (n0 + 63) & ~63LL; n < n1; n += 64) unit_tile[n >> 6] = (int)t;
+    }
+}
+
+// {low 32 bits of the block offset, count} of neighbour entry k of tile t
+__global__ void entries_kernel(const int *nbr, const long long *base, const int *nf,
+                               long long t_n, uint2 *entries) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < t_n * NBR;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long t = i / NBR;
+        const int nb = nbr[i];
+        const long long tt = nb >= 0 ? nb : t;
+        entries[i] = make_uint2((unsigned)base[tt], (unsigned)nf[tt]);
+    }
+}
+
+// one thread per slot: the node word + slot, and the ranks of the 18 pulled
+// values in their source tiles
+__global__ void node_records_kernel(const uint32_t *meta, const int *nbr, long long t_n,
+                                    const long long *base, const unsigned char *rank,
+                                    const int *unit_tile, uint32_t *node_meta,
+                                    uint4 *node_rec) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < t_n * 64;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int r = rank[i];
+        if (r == 255) continue;
+        const long long t = i >> 6;
+        const int j = (int)(i & 63);
+        const long long n = base[t] / Q + r;
+        const uint32_t m = meta[i];
+        node_meta[n] = (m & 0x1ffffffu) | ((uint32_t)j << 25);
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
+        for (int q = 1; q < Q; ++q) {
+            if (!((m >> q) & 1u)) continue;   // bounce-back: reads its own slot
+            const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
+            const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
+            const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);
+            const int dz = sz < 0 ? -1 : (sz > 3 ? 1 : 0);
+            const int k = delta_index(dx, dy, dz);
+            const int nb = k == 13 ? (int)t : nbr[t * NBR + k];
+            const int src = (sx & 3) + 4 * (sy & 3) + 16 * (sz & 3);
+            const uint32_t rs = rank[(long long)nb * 64 + src] & 63u;
+            w[(q - 1) / 5] |= rs << (6 * ((q - 1) % 5));
+        }
+        w[3] |= (uint32_t)r << 18;
+        w[3] |= (uint32_t)(t - unit_tile[n >> 6]) << 24;
+        node_rec[n] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+}  // namespace
+}  // namespace tlbm
+
+extern "C" int tlbm_compact_nodes(const uint32_t *d_meta, const int32_t *d_nbr, int64_t t_n,
+                                  int64_t n_fn, const int64_t *d_base, const int32_t *d_nf,
+                                  const uint8_t *d_rank, uint32_t *d_node_meta,
+                                  uint32_t *d_node_rec, int32_t *d_unit_tile,
+                                  uint32_t *d_entries, void *stream) {
+    if (t_n == 0 || n_fn == 0) return TLBM_OK;
+    if (!d_meta || !d_nbr || !d_base || !d_nf || !d_rank || !d_node_meta || !d_node_rec ||
+        !d_unit_tile || !d_entries || t_n < 0 || n_fn < 0) {
+        set_error("tlbm_compact_nodes: bad argument");
+        return TLBM_ERR_ARG;
+    }
+    if ((long long)Q * n_fn >= (1LL << 32)) {
+        set_error("tlbm_compact_nodes: 19 * n_fn = %lld needs 64-bit offsets",
+                  (long long)Q * n_fn);
+        return TLBM_ERR_ARG;
+    }
+    cudaStream_t s = as_stream(stream);
+    const auto *base = reinterpret_cast<const long long *>(d_base);
+    unit_tile_kernel<<<grid_for_slots(t_n), 256, 0, s>>>(base, d_nf, t_n, d_unit_tile);
+    int rc = launch_check("unit_tile_kernel");
+    if (rc) return rc;
+    entries_kernel<<<grid_for_slots(t_n * NBR), 256, 0, s>>>(
+        d_nbr, base, d_nf, t_n, reinterpret_cast<uint2 *>(d_entries));
+    if ((rc = launch_check("entries_kernel"))) return rc;
+    node_records_kernel<<<grid_for_slots(t_n * 64), 256, 0, s>>>(
+        d_meta, d_nbr, t_n, base, d_rank, d_unit_tile, d_node_meta,
+        reinterpret_cast<uint4 *>(d_node_rec));
+    return launch_check("node_records_kernel");
+}
+
 // ---- slab halo on a compact store (fields.cu: halo_kernel for blocks) -----
 // Same packed buffer as tlbm_halo -- buf[(tile - tile_begin) * 80 + k * 16 +
 // (x + 4 y)] for the 5 directions crossing the outer z plane -- with each

@@ -38,6 +38,9 @@ namespace step_detail {
 #ifndef TLBM_WARPS_COMPACT_F32
 #define TLBM_WARPS_COMPACT_F32 48
 #endif
+#ifndef TLBM_WARPS_NODES_F32
+#define TLBM_WARPS_NODES_F32 48
+#endif
 // per (q, j): 64 * (neighbour-row entry of the source tile) + source slot
 struct CompactPull {
     uint16_t w[Q * 64];
@@ -72,17 +75,129 @@ constexpr int min_blocks_compact() {
            (2 * compact_tiles_per_cta<T>());
 }
 
+// The tail of a node's update on the compact store, shared by the compact
+// kernels: boundary handling, collision, the store into the other copy at
+// own + q * nf_own + rank_own, and the fused halo.
+template <class T, int QUASI, int VARIANT, bool MRT, bool FMA, bool HALO, class Off>
+__device__ __forceinline__ uint32_t compact_finish(const StepParams<T, MRT> &p, long long tile,
+                                                   int j, uint32_t meta, T (&g)[Q], Off own,
+                                                   int nf_own, int rank_own) {
+    uint32_t status = 0;
+    if (VARIANT == TLBM_FULL) {
+        const int tag = meta_type(meta);
+        if (tag == BB_WALL) {
+#pragma unroll
+            for (int q = 1; q < Q; ++q)
+                if (q < opp(q)) { T t = g[q]; g[q] = g[opp(q)]; g[opp(q)] = t; }
+        } else {
+            if (tag == INLET || tag == OUTLET)
+                zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
+            if constexpr (MRT && FMA)
+                status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
+            else if constexpr (MRT)
+                status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
+            else if constexpr (FMA)
+                status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
+            else
+                status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
+        }
+    }
+    T *out = p.dst + own;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
+    if constexpr (HALO) {
+        // fused halo: the neighbour's ghost copy of this tile has the same
+        // nodes (same ranks and count), at its own block offset
+        const int z = j >> 4;
+        if (p.halo_up && z == 3 && tile >= p.halo_up_begin && tile < p.halo_up_end) {
+            T *peer = p.halo_up + p.halo_up_cbase[tile - p.halo_up_begin];
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                peer[up_dir(k) * nf_own + rank_own] = g[up_dir(k)];
+        }
+        if (p.halo_down && z == 0 && tile >= p.halo_down_begin && tile < p.halo_down_end) {
+            T *peer = p.halo_down + p.halo_down_cbase[tile - p.halo_down_begin];
+#pragma unroll
+            for (int k = 0; k < 5; ++k)
+                peer[opp(up_dir(k)) * nf_own + rank_own] = g[opp(up_dir(k))];
+        }
+    }
+    return status;
+}
+
+// a neighbour entry as the update sees it: block offset (unsigned 32-bit
+// from the copy start, or 64-bit) and block length
+template <class Off>
+struct Entry {
+    Off off;
+    int nf;
+};
+
+// One node's update in the tile-parallel compact kernel: pull gather
+// through the staged neighbourhood (rank bytes rank[k * 64 + s] and
+// entry(k) = block offset and length of the 27 neighbour entries, entry 13 =
+// the node's own tile), then compact_finish.  The offset is an unsigned
+// 32-bit element offset from the copy start (OFF32) or a 64-bit one.
+template <class T, int QUASI, int VARIANT, bool MRT, bool FMA, bool HALO, class E>
+__device__ __forceinline__ uint32_t compact_update(const StepParams<T, MRT> &p, long long tile,
+                                                   int j, uint32_t meta,
+                                                   const unsigned char *rank, E entry) {
+    const T *base0 = opaque(p.src);
+    const auto mine = entry(13);
+    const auto own = mine.off;
+    const int nf_own = mine.nf;
+    const int rank_own = rank[13 * 64 + j];
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
+            g[q] = load_ro(base0 + (own + (decltype(own))(q * nf_own + rank_own)));
+            continue;
+        }
+        // w = 64 * (source tile entry) + source slot
+        const uint32_t w = __ldg(&kCompactPull.w[q * 64 + j]);
+        const bool link = (meta >> q) & 1u;
+        const int k = link ? (int)(w >> 6) : 13;
+        const int r = link ? (int)rank[w] : rank_own;
+        const int blk = link ? q : opp(q);
+        const auto e = entry(k);
+        g[q] = load_ro(base0 + (e.off + (decltype(own))(blk * e.nf + r)));
+    }
+    return compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, tile, j, meta, g, own, nf_own,
+                                                             rank_own);
+}
+
+// OR a warp's status bits into the launch's status word (one conditional
+// atomic per warp; see step_kernel)
+template <class P>
+__device__ __forceinline__ void report_status(const P &p, uint32_t status) {
+    if (p.flags) {
+        const uint32_t any = __reduce_or_sync(0xffffffffu, status);
+        if (any && (threadIdx.x & 31) == 0) {
+            uint32_t *f = p.flags;
+            if (p.iter)
+                f += (unsigned long long)(*p.iter + p.iter_add) % p.ring_len;
+            if (any & ~*reinterpret_cast<volatile uint32_t *>(f)) atomicOr(f, any);
+        }
+    }
+}
+
+// no D3Q19 pull reads one of the 8 corner neighbours: they are not staged
+__host__ __device__ constexpr bool corner_entry(int k) {
+    return k == 0 || k == 2 || k == 6 || k == 8 || k == 18 || k == 20 || k == 24 || k == 26;
+}
+
 // OFF32: every element offset of a copy fits 32 bits (19 * n_fn < 2^32, i.e.
 // up to 226 M fluid nodes): neighbour block starts are staged as 32-bit
 // offsets from the copy start and each pull is one 32-bit add chain plus one
 // IMAD.WIDE.U32 from a single base -- fewer live registers than a 64-bit
-// pointer per pull.  Otherwise 64-bit block pointers are staged.
+// offset per pull.
 template <class T, int QUASI, int TABLE, int VARIANT, int TPC, bool MRT, bool FMA, bool OFF32,
           bool ORDERED, bool HALO>
 __global__ void __launch_bounds__(64 * TPC, min_blocks_compact<T, MRT, VARIANT, FMA>())
 step_kernel_compact(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
-    __shared__ const T *s_src[OFF32 ? 1 : TPC][NBR];
+    __shared__ long long s_src[OFF32 ? 1 : TPC][NBR];
     __shared__ unsigned s_off[OFF32 ? TPC : 1][NBR];
     __shared__ int s_nf[TPC][NBR];
     __shared__ __align__(16) unsigned char s_rank[TPC][NBR][64];
@@ -100,14 +215,12 @@ step_kernel_compact(const StepParams<T, MRT> p) {
         const bool ok = pos0 + i / NBR < p.tile_end;
         const long long t = ok ? tile_at<ORDERED>(p, pos0 + i / NBR) : 0;
         const int k = i % NBR;
-        // no D3Q19 pull reads one of the 8 corner neighbours: not staged
-        if (k == 0 || k == 2 || k == 6 || k == 8 || k == 18 || k == 20 || k == 24 || k == 26)
-            continue;
+        if (corner_entry(k)) continue;
         long long nb = -1;
         if (ok) nb = VARIANT == TLBM_READ_WRITE_ONLY ? (k == 13 ? t : -1) : p.nbr[t * NBR + k];
         const long long tt = nb >= 0 ? nb : t;
         if (OFF32) s_off[OFF32 ? i / NBR : 0][k] = (unsigned)p.cbase[tt];
-        else s_src[OFF32 ? 0 : i / NBR][k] = p.src + p.cbase[tt];
+        else s_src[OFF32 ? 0 : i / NBR][k] = p.cbase[tt];
         s_nf[i / NBR][k] = p.cnf[tt];
         const uint4 *r = reinterpret_cast<const uint4 *>(p.crank + tt * 64);
         uint4 *d = reinterpret_cast<uint4 *>(&s_rank[i / NBR][k][0]);
@@ -118,84 +231,79 @@ step_kernel_compact(const StepParams<T, MRT> p) {
 
     uint32_t status = 0;
     if (meta & META_ACTIVE) {
+        if constexpr (OFF32)
+            status = compact_update<T, QUASI, VARIANT, MRT, FMA, HALO>(
+                p, tile, j, meta, &s_rank[ti][0][0],
+                [&](int k) { return Entry<unsigned>{s_off[ti][k], s_nf[ti][k]}; });
+        else
+            status = compact_update<T, QUASI, VARIANT, MRT, FMA, HALO>(
+                p, tile, j, meta, &s_rank[ti][0][0],
+                [&](int k) { return Entry<long long>{s_src[ti][k], s_nf[ti][k]}; });
+    }
+    report_status(p, status);
+}
+
+// ---- node-parallel compact step -------------------------------------------
+// One thread per non-solid node, in store order, so the lanes a partly solid
+// tile leaves idle in the tile-parallel kernel (a third at porosity 0.2) do
+// work.  Each node's pull sources come from its precomputed record
+// (tlbm_compact_nodes): the 18 source ranks, its own rank and its tile; the
+// source tile's block offset and length come from the tile's 27-entry row of
+// {offset, count} (8-byte loads that the lanes of one tile share in L1);
+// which entry a pull reads is the compile-time pull table.  Node-level
+// metadata is 20 B + 216 B per tile (~25 B per fluid node at porosity 0.2,
+// 8% of the 304 B the populations move in fp64).
+#ifndef TLBM_NODES_THREADS
+#define TLBM_NODES_THREADS 128
+#endif
+template <class T, bool MRT, bool FMA = false>
+constexpr int min_blocks_nodes() {
+    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32
+                                  : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
+                : (sizeof(T) == 4 ? TLBM_WARPS_NODES_F32 : TLBM_WARPS_COMPACT)) /
+           (TLBM_NODES_THREADS / 32);
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA, bool HALO>
+__global__ void __launch_bounds__(TLBM_NODES_THREADS, min_blocks_nodes<T, MRT, FMA>())
+step_kernel_nodes(const StepParams<T, MRT> p) {
+    static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
+    const long long n = p.node_begin + (long long)blockIdx.x * TLBM_NODES_THREADS + threadIdx.x;
+    uint32_t status = 0;
+    if (n < p.node_end) {
+        const uint32_t meta = __ldg(p.node_meta + n);
+        const uint4 rec = __ldg(reinterpret_cast<const uint4 *>(p.node_rec) + n);
+        const int j = (int)(meta >> 25);
+        const int rank_own = (int)((rec.w >> 18) & 63u);
+        const long long tile = (long long)__ldg(p.unit_tile + (n >> 6)) + ((rec.w >> 24) & 63u);
+        const uint2 *ent = reinterpret_cast<const uint2 *>(p.entries) + tile * NBR;
+        const uint2 mine = __ldg(ent + 13);
+        const unsigned own = mine.x;
+        const int nf_own = (int)mine.y;
         const T *base0 = opaque(p.src);
-        const T *own_src = OFF32 ? base0 + s_off[OFF32 ? ti : 0][13]
-                                 : s_src[OFF32 ? 0 : ti][13];
-        const int nf_own = s_nf[ti][13];
-        const int rank_own = s_rank[ti][13][j];
         T g[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
-                if (OFF32)
-                    g[q] = load_ro(base0 + (s_off[OFF32 ? ti : 0][13] +
-                                            (unsigned)(q * nf_own + rank_own)));
-                else
-                    g[q] = load_ro(own_src + (q * nf_own + rank_own));
+                g[q] = load_ro(base0 + (own + (unsigned)(q * nf_own + rank_own)));
                 continue;
             }
-            // w = 64 * (source tile entry) + source slot
-            const uint32_t w = __ldg(&kCompactPull.w[q * 64 + j]);
+            const uint32_t word = (q - 1) < 5 ? rec.x : (q - 1) < 10 ? rec.y
+                                : (q - 1) < 15 ? rec.z : rec.w;
+            const int rs = (int)((word >> (6 * ((q - 1) % 5))) & 63u);
+            // no link: halfway bounce-back reads the node's own slot of
+            // block opp(q) (entry 13 is the own tile)
             const bool link = (meta >> q) & 1u;
-            const int k = link ? (int)(w >> 6) : 13;
-            const int rank = link ? (int)(&s_rank[ti][0][0])[w] : rank_own;
+            const int k = link ? (int)(__ldg(&kCompactPull.w[q * 64 + j]) >> 6) : 13;
+            const uint2 e = __ldg(ent + k);
             const int blk = link ? q : opp(q);
-            if (OFF32)
-                g[q] = load_ro(base0 + (s_off[OFF32 ? ti : 0][k] +
-                                        (unsigned)(blk * s_nf[ti][k] + rank)));
-            else
-                g[q] = load_ro(s_src[OFF32 ? 0 : ti][k] + (blk * s_nf[ti][k] + rank));
+            const int r = link ? rs : rank_own;
+            g[q] = load_ro(base0 + (e.x + (unsigned)(blk * (int)e.y + r)));
         }
-
-        if (VARIANT == TLBM_FULL) {
-            const int tag = meta_type(meta);
-            if (tag == BB_WALL) {
-#pragma unroll
-                for (int q = 1; q < Q; ++q)
-                    if (q < opp(q)) { T t = g[q]; g[q] = g[opp(q)]; g[opp(q)] = t; }
-            } else {
-                if (tag == INLET || tag == OUTLET)
-                    zou_he<T, QUASI>(g, tag, meta_face(meta), p.inlet_u, p.outlet_rho);
-                if constexpr (MRT && FMA)
-                    status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
-                else if constexpr (MRT)
-                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
-                else if constexpr (FMA)
-                    status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
-                else
-                    status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
-            }
-        }
-        T *out = p.dst + (own_src - p.src);
-#pragma unroll
-        for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
-        if constexpr (HALO) {
-            // fused halo: the neighbour's ghost copy of this tile has the same
-            // nodes (same ranks and count), at its own block offset
-            const int z = j >> 4;
-            if (p.halo_up && z == 3 && tile >= p.halo_up_begin && tile < p.halo_up_end) {
-                T *peer = p.halo_up + p.halo_up_cbase[tile - p.halo_up_begin];
-#pragma unroll
-                for (int k = 0; k < 5; ++k)
-                    peer[up_dir(k) * nf_own + rank_own] = g[up_dir(k)];
-            }
-            if (p.halo_down && z == 0 && tile >= p.halo_down_begin && tile < p.halo_down_end) {
-                T *peer = p.halo_down + p.halo_down_cbase[tile - p.halo_down_begin];
-#pragma unroll
-                for (int k = 0; k < 5; ++k)
-                    peer[opp(up_dir(k)) * nf_own + rank_own] = g[opp(up_dir(k))];
-            }
-        }
+        status = compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, tile, j, meta, g, own,
+                                                                   nf_own, rank_own);
     }
-    if (p.flags) {
-        const uint32_t any = __reduce_or_sync(0xffffffffu, status);
-        if (any && (threadIdx.x & 31) == 0) {
-            uint32_t *f = p.flags;
-            if (p.iter)
-                f += (unsigned long long)(*p.iter + p.iter_add) % p.ring_len;
-            if (any & ~*reinterpret_cast<volatile uint32_t *>(f)) atomicOr(f, any);
-        }
-    }
+    report_status(p, status);
 }
 
 }  // namespace step_detail

@@ -65,6 +65,12 @@ struct StepParams {
     // fused halo on compact storage: neighbour block offsets of its ghosts
     const long long *halo_up_cbase;
     const long long *halo_down_cbase;
+    // node-parallel compact step (step_kernel_nodes); node_meta null otherwise
+    const uint32_t *__restrict__ node_meta;
+    const void *__restrict__ node_rec;
+    const int *__restrict__ unit_tile;
+    const void *__restrict__ entries;
+    long long node_begin, node_end;
 };
 
 // the tile at launch position pos (tile_begin <= pos < tile_end); ORDERED
@@ -419,6 +425,22 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
 }
 
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA>
+int launch_nodes(const tlbm_step_args *a, cudaStream_t s) {
+    StepParams<T, MRT> p;
+    fill_params<T, MRT, FMA>(p, a);
+    const long long n = a->node_end - a->node_begin;
+    if (n <= 0) return TLBM_OK;
+    const unsigned grid = (unsigned)((n + TLBM_NODES_THREADS - 1) / TLBM_NODES_THREADS);
+    if (VARIANT == TLBM_FULL && (a->halo_up || a->halo_down))
+        step_kernel_nodes<T, QUASI, TABLE, VARIANT, MRT, FMA, VARIANT == TLBM_FULL>
+            <<<grid, TLBM_NODES_THREADS, 0, s>>>(p);
+    else
+        step_kernel_nodes<T, QUASI, TABLE, VARIANT, MRT, FMA, false>
+            <<<grid, TLBM_NODES_THREADS, 0, s>>>(p);
+    return launch_check("step_kernel_nodes");
+}
+
+template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA>
 int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
     fill_params<T, MRT, FMA>(p, a);
@@ -469,6 +491,16 @@ int launch_compact(const tlbm_step_args *a, cudaStream_t s) {
         return TLBM_ERR_ARG;
     }
     constexpr bool kFma = VARIANT == TLBM_FULL && sizeof(T) == 8;
+    if (a->node_meta) {
+        if (!a->node_rec || !a->unit_tile || !a->entries || !a->rel32 || a->order ||
+            a->node_begin < 0 || a->node_end < a->node_begin) {
+            set_error("tlbm_step: the node-parallel step needs node_rec, unit_tile, entries, "
+                      "a node range, 32-bit offsets (rel32) and tile order");
+            return TLBM_ERR_ARG;
+        }
+        if (kFma && fma_path(a, MRT)) return launch_nodes<T, QUASI, TABLE, VARIANT, MRT, kFma>(a, s);
+        return launch_nodes<T, QUASI, TABLE, VARIANT, MRT, false>(a, s);
+    }
     if (kFma && fma_path(a, MRT))
         return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, kFma>(a, s);
     return launch_compact_as<T, QUASI, TABLE, VARIANT, MRT, false>(a, s);
@@ -571,6 +603,12 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     p.order = a->order;
     p.halo_up_cbase = reinterpret_cast<const long long *>(a->halo_up_cbase);
     p.halo_down_cbase = reinterpret_cast<const long long *>(a->halo_down_cbase);
+    p.node_meta = a->node_meta;
+    p.node_rec = a->node_rec;
+    p.unit_tile = a->unit_tile;
+    p.entries = a->entries;
+    p.node_begin = a->node_begin;
+    p.node_end = a->node_end;
 }
 
 template <class T>

@@ -225,6 +225,34 @@ class CompactFieldStore(FieldStore):
                  nat.stream_ptr(self.device))
         self.flat = torch.empty(2 * Q * self.n_fn, dtype=self.tdtype, device=self.device)
 
+    def node_records(self, tiling):
+        """Per-node records for the node-parallel step (tlbm_compact_nodes):
+        ``node_meta`` (n_fn,) int32, ``node_rec`` (n_fn, 4) int32, ``unit_tile``
+        (ceil(n_fn / 64),) int32 and ``entries`` (t_n, 27, 2) int32 -- 20 B
+        per node + 216 B per tile; built once and cached."""
+        if getattr(self, "_nodes", None) is None:
+            dev = self.device
+            n = max(self.n_fn, 1)
+            rec = {"node_meta": torch.empty(n, dtype=torch.int32, device=dev),
+                   "node_rec": torch.empty((n, 4), dtype=torch.int32, device=dev),
+                   "unit_tile": torch.empty((n + 63) // 64, dtype=torch.int32, device=dev),
+                   "entries": torch.empty((max(self.t_n, 1), 27, 2), dtype=torch.int32,
+                                          device=dev)}
+            nat.call("tlbm_compact_nodes", nat.ptr(tiling.meta), nat.ptr(tiling.nbr), self.t_n,
+                     self.n_fn, nat.ptr(self.base), nat.ptr(self.nf), nat.ptr(self.rank),
+                     nat.ptr(rec["node_meta"]), nat.ptr(rec["node_rec"]),
+                     nat.ptr(rec["unit_tile"]), nat.ptr(rec["entries"]),
+                     nat.stream_ptr(dev))
+            self._nodes = rec
+        return self._nodes
+
+    def node_range(self, tile_begin, tile_end):
+        """Store-order node range [n0, n1) of tiles [tile_begin, tile_end)."""
+        if getattr(self, "_node_prefix", None) is None:
+            self._node_prefix = np.concatenate(
+                [(self.base // Q).cpu().numpy(), [self.n_fn]]).astype(np.int64)
+        return int(self._node_prefix[tile_begin]), int(self._node_prefix[tile_end])
+
     def copy_tensor(self, copy):
         if int(copy) not in (0, 1):
             raise ValueError(f"copy flag must be 0 or 1: {copy}")

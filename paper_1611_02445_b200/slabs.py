@@ -33,7 +33,8 @@ import torch
 
 from . import _native as nat
 from .geometry import Geometry
-from .solver import SimulationConfig, Solver
+from .solver import SimulationConfig, Solver, use_nodes
+from .tiling import DeviceTiling
 
 TILE = 4
 
@@ -141,7 +142,10 @@ def resolve_auto_storage_global(config, geometry):
 class SlabSolver:
     """One rank's slab: a local Solver plus the halo bookkeeping."""
 
-    def __init__(self, geometry, plan, rank, config=None, device=None):
+    def __init__(self, geometry, plan, rank, config=None, device=None, traversal="auto"):
+        """``traversal``: "tile" (tile-parallel step), "nodes" (node-parallel
+        step over the nodes of each launched tile range; compact storage) or
+        "auto" (solver.use_nodes)."""
         self.plan, self.rank = plan, rank
         self.range = plan.ranges[rank]
         self.local_geometry = plan.local_geometry(geometry, rank)
@@ -150,9 +154,15 @@ class SlabSolver:
             # the neighbour's store): decide on the whole geometry
             config = resolve_auto_storage_global(config, geometry)
         # slab launches name tile ranges (boundary layers, interior), so the
-        # solver keeps the tile-list order
-        self.solver = Solver(self.local_geometry, config or SimulationConfig(), device,
-                             traversal="tile")
+        # solver keeps the tile-list order (or runs node-parallel over the
+        # nodes of those ranges)
+        config = config or SimulationConfig()
+        tiling = DeviceTiling(self.local_geometry, device)
+        if traversal not in ("tile", "nodes"):
+            traversal = ("nodes" if use_nodes(config, tiling.n_fn, tiling.t_n, "auto")
+                         else "tile")
+        self.solver = Solver(self.local_geometry, config, device, tiling=tiling,
+                             traversal=traversal)
         s = self.solver
         layers = layer_tile_ranges(s.tiling.tile_map)
         has_lo, has_hi = self.range.lower >= 0, self.range.upper >= 0
@@ -182,6 +192,8 @@ class SlabSolver:
             s = self.solver
             a = s._args
             a.tile_begin, a.tile_end = rng
+            if s.nodes is not None:
+                a.node_begin, a.node_end = s.store.node_range(*rng)
             a.f_src = s._copies[s.parity]
             a.f_dst = s._copies[1 - s.parity]
             a.flags = s.status.data_ptr() + 4 * (s.iteration % len(s.status))
@@ -519,9 +531,10 @@ class DistributedSlabRunner:
     interior-tile launch.  ``transport="gloo"`` stages the halo through host
     memory instead (tests with several ranks on one GPU)."""
 
-    def __init__(self, geometry, world, rank, config=None, device=None, transport="nccl"):
+    def __init__(self, geometry, world, rank, config=None, device=None, transport="nccl",
+                 traversal="auto"):
         self.plan = SlabPlan(geometry, world)
-        self.slab = SlabSolver(geometry, self.plan, rank, config, device)
+        self.slab = SlabSolver(geometry, self.plan, rank, config, device, traversal)
         self.transport = transport
         self.ipc = None
         self.halo = None
@@ -610,9 +623,11 @@ class VirtualSlabs:
     peer mappings; slabs run one after another on one stream, so no step
     counters are needed (scripts/halo_overhead.py times this path)."""
 
-    def __init__(self, geometry, world, config=None, device=None, fused=False):
+    def __init__(self, geometry, world, config=None, device=None, fused=False,
+                 traversal="auto"):
         self.plan = SlabPlan(geometry, world)
-        self.slabs = [SlabSolver(geometry, self.plan, r, config, device) for r in range(world)]
+        self.slabs = [SlabSolver(geometry, self.plan, r, config, device, traversal)
+                      for r in range(world)]
         self.fused = bool(fused)
     def _exchange(self):
         for sl in self.slabs:

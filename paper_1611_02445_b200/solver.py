@@ -144,7 +144,11 @@ class Solver:
         lines across z and lose DRAM streaming locality in the blocked order
         (0.974 -> 0.945), so they keep the tile order, as does compact
         storage (measured slower).  An int forces the
-        blocking with that many tile rows."""
+        blocking with that many tile rows.  "nodes" (compact storage only)
+        runs the node-parallel step: one thread per non-solid node in store
+        order instead of one per tile slot (csrc/step_compact.cuh:
+        step_kernel_nodes); "auto" picks it for compact storage below tile
+        utilisation AUTO_NODES_ETA."""
         self.config = config if config is not None else SimulationConfig()
         self.geometry = geometry
         self.tiling = tiling if tiling is not None else DeviceTiling(geometry, device)
@@ -194,6 +198,18 @@ class Solver:
         else:
             a.collision = nat.LBGK
         self._copies = (self.store.copy_tensor(0).data_ptr(), self.store.copy_tensor(1).data_ptr())
+        self.nodes = None
+        if use_nodes(self.config, self.n_fn, self.t_n, traversal):
+            if not a.rel32:
+                raise ValueError("the node-parallel step needs 32-bit offsets "
+                                 "(19 * n_fn < 2^32)")
+            self.nodes = self.store.node_records(self.tiling)
+            a.node_meta = self.nodes["node_meta"].data_ptr()
+            a.node_rec = self.nodes["node_rec"].data_ptr()
+            a.unit_tile = self.nodes["unit_tile"].data_ptr()
+            a.entries = self.nodes["entries"].data_ptr()
+            a.node_begin, a.node_end = 0, self.n_fn
+            traversal = "tile"
         self.order = traversal_order(self.tiling, self.store, traversal)
         a.order = self.order.data_ptr() if self.order is not None else None
         self._graphs = {}
@@ -274,6 +290,7 @@ class Solver:
         a = self._args
         a.variant = int(variant)
         a.tile_begin, a.tile_end = 0, self.t_n
+        a.node_begin, a.node_end = 0, self.n_fn
         a.iter_counter = None
         stream = nat.stream_ptr(self.device)
         lib = nat.load()
@@ -316,6 +333,7 @@ class Solver:
         nat.ctypes.memmove(ctypes_copy, nat.ctypes.byref(self._args), nat.ctypes.sizeof(a))
         a.variant = variant
         a.tile_begin, a.tile_end = 0, self.t_n
+        a.node_begin, a.node_end = 0, self.n_fn
         a.flags = self.status.data_ptr()
         a.iter_counter = self._iter_dev.data_ptr()
         a.ring_len = STATUS_RING
@@ -574,6 +592,22 @@ def traversal_order(tiling, store, traversal="auto"):
     tx, ty, tz = coords[:, 0], coords[:, 1], coords[:, 2]
     key = (((ty // yb) * ntz + tz) * nty + ty) * ntx + tx
     return torch.argsort(key, stable=True).to(torch.int32)
+
+
+# traversal="auto" on compact storage: the node-parallel step below this
+# tile utilisation (placeholder until measured)
+AUTO_NODES_ETA = 0.0
+
+
+def use_nodes(config, n_fn, t_n, traversal):
+    """Does a solver with this configuration run the node-parallel step?"""
+    if traversal == "nodes":
+        if config.storage != "compact":
+            raise ValueError("traversal='nodes' needs storage='compact'")
+        return True
+    if traversal != "auto" or config.storage != "compact" or not t_n:
+        return False
+    return n_fn / (64.0 * t_n) < AUTO_NODES_ETA
 
 
 # storage="auto": compact below this tile utilisation (fp64).  From the

@@ -1,0 +1,26 @@
+#!/bin/bash
+# Node-parallel compact step (traversal="nodes", step_kernel_nodes): parity
+# (compact, slabs), then porosity sweep blocks / compact / nodes, ncu of the
+# nodes kernel at porosity 0.2 (fp64, fp32).
+set -u
+O=gpurun_out/exp43
+mkdir -p $O
+timeout 1200 python -m pytest tests/test_gpu_compact.py tests/test_gpu_slabs.py -m gpu -q -x > $O/pytest.txt 2>&1
+tail -3 $O/pytest.txt
+for r in 1 2; do
+  timeout 900 python scripts/porosity_sweep.py --porosities 0.2,0.3,0.5,0.7,0.9,1.0 --precisions f64,f32 --storages compact,nodes,blocks --steps 20 > $O/sweep_$r.jsonl 2>$O/sweep_$r.err
+done
+for pr in f64 f32; do
+  ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 5 -c 1 \
+    -o $O/prof_nodes_${pr}_p02 python scripts/porosity_sweep.py --porosities 0.2 --precisions $pr --storages nodes --steps 3 --warmup 5 > /dev/null 2>&1
+  ncu -i $O/prof_nodes_${pr}_p02.ncu-rep --page details > $O/prof_nodes_${pr}_p02_details.txt 2>&1
+  ncu -i $O/prof_nodes_${pr}_p02.ncu-rep --page raw --csv > $O/prof_nodes_${pr}_p02_raw.csv 2>&1
+  ncu -i $O/prof_nodes_${pr}_p02.ncu-rep --page source --csv > $O/prof_nodes_${pr}_p02_source.csv 2>&1
+  rm -f $O/prof_nodes_${pr}_p02.ncu-rep
+done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/exp43/sweep_*.jsonl')):
+    for l in open(f):
+        d=json.loads(l); print(f.split('/')[-1], d['case'], d['precision'], d['storage'], round(d['ms_per_step'],4), round(d['bu'],4))
+PY

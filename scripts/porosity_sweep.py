@@ -30,9 +30,12 @@ def hbm_gbs():
 
 def time_case(name, geo, precision, steps, warmup, table, storage="blocks"):
     t0 = time.perf_counter()
+    # "nodes": compact storage, node-parallel step; "compact": compact
+    # storage, tile-parallel step; "auto": what the solver picks
     cfg = SimulationConfig(tau=workloads.TAU, precision=precision, table=table,
-                           u_max_guard=0.0, storage=storage)
-    s = Solver(geo, cfg)
+                           u_max_guard=0.0, storage="compact" if storage == "nodes" else storage)
+    s = Solver(geo, cfg, traversal="nodes" if storage == "nodes"
+               else ("tile" if storage == "compact" else "auto"))
     setup = time.perf_counter() - t0
     s.step(warmup, check=False)
     torch.cuda.synchronize()
@@ -47,6 +50,7 @@ def time_case(name, geo, precision, steps, warmup, table, storage="blocks"):
     mlups = s.n_fn / (ms / 1e3) / 1e6
     rec = {"case": name, "precision": precision, "table": s.config.table.value,
            "storage": storage, "storage_used": s.config.storage,
+           "traversal_used": "nodes" if s.nodes is not None else "tile",
            "dims": list(geo.shape),
            "porosity": geo.porosity(), "t_n": s.t_n, "n_fn": s.n_fn,
            "eta_t": s.n_fn / (64 * s.t_n), "ms_per_step": ms, "mlups": mlups,
@@ -67,7 +71,7 @@ def main():
     p.add_argument("--vessel", action="store_true")
     p.add_argument("--cavity", action="store_true")
     p.add_argument("--l2-fetch", type=int, default=-1)
-    p.add_argument("--storages", default="blocks", help="comma list of blocks,compact,auto")
+    p.add_argument("--storages", default="blocks", help="comma list of blocks,compact,nodes,auto")
     a = p.parse_args()
     if a.l2_fetch >= 0:
         from paper_1611_02445_b200 import _native as nat

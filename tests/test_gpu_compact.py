@@ -14,11 +14,12 @@ from paper_1611_02445_b200 import geometry, layout, slabs, solver
 from test_gpu_step import DTYPES, MODELS, compare, oracle_run, perturbed_eq
 
 pytestmark = pytest.mark.gpu
-def make(geo, m=MODELS["inc"], dt=np.float64, table=None, f0=None, storage="compact", **kw):
+def make(geo, m=MODELS["inc"], dt=np.float64, table=None, f0=None, storage="compact",
+         traversal="tile", **kw):
     cfg = solver.SimulationConfig(fluid=m, tau=0.6, u_max_guard=0.0, table=table,
                                   precision="f64" if dt == np.float64 else "f32",
                                   storage=storage, **kw)
-    s = solver.Solver(geo, cfg)
+    s = solver.Solver(geo, cfg, traversal=traversal)
     if f0 is not None:
         s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
     return s
@@ -45,19 +46,22 @@ def test_rejects_unsupported_configs():
         solver.SimulationConfig(storage="sparse")
 
 
+@pytest.mark.parametrize("traversal", ["tile", "nodes"])
 @pytest.mark.parametrize("dn", DTYPES)
-def test_cavity64_1000_steps_compact(c_oracle, dn):
+def test_cavity64_1000_steps_compact(c_oracle, dn, traversal):
     dt = DTYPES[dn]
     geo = geometry.generate_cavity3d(64)
     m = MODELS["inc"]
-    s = make(geo, m, dt)
+    s = make(geo, m, dt, traversal=traversal)
+    assert (s.nodes is not None) == (traversal == "nodes")
     s.run(1000)
     compare(s, oracle_run(c_oracle, geo, m, dt, dense.init_equilibrium(geo.shape, m, dt), 1000),
             dt)
 
 
+@pytest.mark.parametrize("traversal", ["tile", "nodes"])
 @pytest.mark.parametrize("seed", range(6))
-def test_random_geometries_compact(c_oracle, seed):
+def test_random_geometries_compact(c_oracle, seed, traversal):
     """Mixed solid / fluid / bounce-back / inlet / outlet geometries, both
     dtypes and fluid models: bit-exact vs the oracle."""
     rng = np.random.default_rng(1300 + seed)
@@ -68,7 +72,7 @@ def test_random_geometries_compact(c_oracle, seed):
         for m in MODELS.values():
             f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), seed)
             want = oracle_run(c_oracle, geo, m, dt, f0, 15)
-            s = make(geo, m, dt, None, f0)
+            s = make(geo, m, dt, None, f0, traversal=traversal)
             s.step(15)
             compare(s, want, dt)
 
@@ -81,17 +85,18 @@ def test_compact_equals_blocks(kw):
     compact one): identical canonical fields and macroscopic readout."""
     geo = geometry.generate_sphere_pack(32, 8, 0.45, seed=6, inlet_velocity=(0, 0, 0.02))
     runs = []
-    for storage in ("blocks", "compact"):
+    for storage, trav in (("blocks", "tile"), ("compact", "tile"), ("compact", "nodes")):
         cfg = solver.SimulationConfig(tau=0.6, u_max_guard=0.0, storage=storage,
                                       **({"fluid": "incompressible"} | kw))
-        s = solver.Solver(geo, cfg)
+        s = solver.Solver(geo, cfg, traversal=trav)
         s.init_equilibrium(1.0, (0.0, 0.0, 0.01))
         s.step(70, graph=(storage == "compact"))
         mask = s.nonsolid_mask(device=True)
         rho, u, _ = s.macroscopic(device=True)
         runs.append((s.fields_canonical(device=True)[:, mask], rho[mask], u[:, mask]))
-    for a, b in zip(*runs):
-        assert torch.equal(a, b)
+    for other in runs[1:]:
+        for a, b in zip(runs[0], other):
+            assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("variant", [nat.PROPAGATION_ONLY, nat.READ_WRITE_ONLY])
@@ -99,11 +104,11 @@ def test_ladder_variants_compact(variant):
     geo = geometry.generate_sphere_pack(24, 6, 0.5, seed=2, inlet_velocity=(0, 0, 0.01))
     f0 = perturbed_eq(geo.shape, MODELS["inc"], np.float64, seed=5)
     runs = []
-    for storage in ("blocks", "compact"):
-        s = make(geo, f0=f0, storage=storage)
+    for storage, trav in (("blocks", "tile"), ("compact", "tile"), ("compact", "nodes")):
+        s = make(geo, f0=f0, storage=storage, traversal=trav)
         s.step(3, variant=variant)
         runs.append(s.fields_canonical(device=True)[:, s.nonsolid_mask(device=True)])
-    assert torch.equal(runs[0], runs[1])
+    assert torch.equal(runs[0], runs[1]) and torch.equal(runs[0], runs[2])
 
 
 def test_checkpoint_across_storages(tmp_path):
@@ -125,3 +130,53 @@ def test_auto_storage_picks_by_tile_utilisation():
     cfg = solver.SimulationConfig(storage="auto", u_max_guard=0.0)
     assert solver.Solver(sparse, cfg).config.storage == "compact"
     assert solver.Solver(dense, cfg).config.storage == "blocks"
+
+
+def test_node_records_decode():
+    """tlbm_compact_nodes records (include/tlbm.h) decoded on the host agree
+    with the store's base / count / ranks and the neighbour map: node n of
+    tile t at rank r is n = base[t] / 19 + r, its word is the tile's node
+    word | slot << 25, and its 18 source ranks are the ranks of the pulled
+    slots in their source tiles."""
+    from paper_1611_02445_b200 import lattice
+    geo = geometry.generate_sphere_pack(24, 6, 0.35, seed=4, inlet_velocity=(0, 0, 0.01))
+    s = make(geo, traversal="nodes")
+    rec = {k: v.cpu().numpy() for k, v in s.nodes.items()}
+    base = s.store.base.cpu().numpy() // 19
+    nf = s.store.nf.cpu().numpy()
+    rank = s.store.rank.cpu().numpy()
+    meta = s.tiling.meta.cpu().numpy().view(np.uint32).reshape(-1)
+    nbr = s.tiling.nbr.cpu().numpy()
+    ent = rec["entries"].view(np.uint32)
+    nm_ = rec["node_meta"].view(np.uint32)
+    nr = rec["node_rec"].view(np.uint32)
+    e = np.asarray(lattice.E_VECTORS)
+    checked = 0
+    for t in range(0, s.t_n, max(1, s.t_n // 60)):
+        for k in range(27):
+            nb = nbr[t, k]
+            tt = nb if nb >= 0 else t
+            assert ent[t, k, 0] == (base[tt] * 19) & 0xffffffff and ent[t, k, 1] == nf[tt]
+        for j in range(64):
+            r = rank[t, j]
+            if r == 255:
+                continue
+            n = base[t] + r
+            m = meta[t * 64 + j]
+            assert nm_[n] == (m & 0x1ffffff) | (j << 25)
+            w = nr[n]
+            assert (w[3] >> 18) & 63 == r
+            assert rec["unit_tile"][n >> 6] + ((w[3] >> 24) & 63) == t
+            x, y, z = j & 3, (j >> 2) & 3, j >> 4
+            for q in range(1, 19):
+                if not (m >> q) & 1:
+                    continue
+                sx, sy, sz = x - e[q][0], y - e[q][1], z - e[q][2]
+                d = [(-1 if v < 0 else (1 if v > 3 else 0)) for v in (sx, sy, sz)]
+                kk = 9 * (d[0] + 1) + 3 * (d[1] + 1) + (d[2] + 1)
+                src_t = t if kk == 13 else nbr[t, kk]
+                src = (sx & 3) + 4 * (sy & 3) + 16 * (sz & 3)
+                got = (w[(q - 1) // 5] >> (6 * ((q - 1) % 5))) & 63
+                assert got == rank[src_t, src]
+            checked += 1
+    assert checked > 100

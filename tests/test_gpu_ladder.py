@@ -1,0 +1,51 @@
+"""SPEC acceptance 11 (the paper's Fig. 11
+ordering): on the cavity 100^3, read/write-only >= propagation-only >= LBGK
+>= MRT in MFLUPS, and utilisation is computed from B_node = 304 bytes
+(txmodel.b_node).  Each rung is timed with CUDA events over graph replays
+(64-step blocks), best of three; a rung may tie the one above it within
+TIE (the two memory-bound rungs differ by ~2% at this size)."""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_1611_02445_b200 import _native as nat
+from paper_1611_02445_b200 import geometry, solver, txmodel
+
+pytestmark = pytest.mark.gpu
+TIE = 0.03
+
+
+def _mflups(s, variant, blocks=8):
+    s.step(solver.GRAPH_STEPS, variant=variant, graph=True)    # capture + warm up
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        s.step(blocks * solver.GRAPH_STEPS, variant=variant, graph=True, check=False)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3 / (blocks * solver.GRAPH_STEPS))
+    s.check()
+    return s.n_fn / best / 1e6
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_ladder_ordering_cavity100(precision):
+    geo = geometry.generate_cavity3d(100)
+    lbgk = solver.Solver(geo, solver.SimulationConfig(tau=0.6, precision=precision,
+                                                      u_max_guard=0.0))
+    mrt = solver.Solver(geo, solver.SimulationConfig(tau=0.6, precision=precision,
+                                                     collision="mrt", u_max_guard=0.0))
+    rw = _mflups(lbgk, nat.READ_WRITE_ONLY)
+    prop = _mflups(lbgk, nat.PROPAGATION_ONLY)
+    full = _mflups(lbgk, nat.FULL)
+    m = _mflups(mrt, nat.FULL)
+    ladder = [rw, prop, full, m]
+    for hi, lo in zip(ladder, ladder[1:]):
+        assert hi >= lo * (1 - TIE), f"ladder out of order: {ladder}"
+    # utilisation as the paper computes it: MFLUPS * B_node / bandwidth
+    b_node = txmodel.b_node(19, 8 if precision == "f64" else 4)
+    assert b_node == (304 if precision == "f64" else 152)
+    assert np.isfinite(lbgk.fields_canonical()).all()

@@ -106,7 +106,16 @@ COLLISIONS = {"lbgk": {}, "mrt": {"collision": "mrt"},
               "lbgk_fma_quasi": {"arithmetic": "fma", "fluid": "quasi-compressible"},
               "compact": {"storage": "compact"},
               "compact_f32_mrt": {"storage": "compact", "precision": "f32", "collision": "mrt"},
+              "compact_nodes": {"storage": "compact", "traversal": "nodes"},
+              "compact_nodes_f32_mrt": {"storage": "compact", "precision": "f32",
+                                        "collision": "mrt", "traversal": "nodes"},
               "auto": {"storage": "auto"}}
+
+
+def _split(coll):
+    """SimulationConfig kwargs and the slab traversal of a COLLISIONS entry."""
+    kw = dict(COLLISIONS[coll])
+    return kw, kw.pop("traversal", "auto")
 
 
 @pytest.mark.parametrize("fused", [False, True])
@@ -117,7 +126,8 @@ def test_virtual_slabs_collision_modes(name, coll, fused):
     decomposition (halo pack/unpack, or the fused peer stores): bit-identical
     to the single-domain step with the same configuration."""
     geo = CASES[name]()
-    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
+    kw, trav = _split(coll)
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **kw)
     if cfg.storage == "auto":
         cfg = slabs.resolve_auto_storage_global(cfg, geo)
     f0 = _f0(geo, cfg.dtype)
@@ -125,7 +135,8 @@ def test_virtual_slabs_collision_modes(name, coll, fused):
     ref.set_fields_canonical(dense.to_canonical(f0, ref.tile_grid.non_empty, np.zeros(19)))
     ref.step(8)
     want = ref.to_dense(ref.fields_canonical(device=True))
-    vs = slabs.VirtualSlabs(geo, 3, cfg, fused=fused)
+    vs = slabs.VirtualSlabs(geo, 3, cfg, fused=fused, traversal=trav)
+    assert all((sl.solver.nodes is not None) == (trav == "nodes") for sl in vs.slabs)
     for sl in vs.slabs:
         s = sl.solver
         fl = _local_f(f0, sl.range, geo.shape[2])
@@ -148,8 +159,10 @@ def _mp_worker(rank, world, port, steps, out, transport="gloo", coll="lbgk"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     geo = CASES["pack_io"]()
-    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
-    run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport=transport)
+    kw, trav = _split(coll)
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **kw)
+    run = slabs.DistributedSlabRunner(geo, world, rank, cfg, transport=transport,
+                                      traversal=trav)
     s = run.slab.solver
     f0 = _f0(geo, np.float64)
     fl = _local_f(f0, run.slab.range, geo.shape[2])
@@ -171,7 +184,7 @@ def _mp_worker(rank, world, port, steps, out, transport="gloo", coll="lbgk"):
 
 @pytest.mark.parametrize("transport,coll", [("gloo", "lbgk"), ("ipc", "lbgk"), ("ipc", "mrt"),
                                             ("ipc", "mrt_fma"), ("ipc", "compact"),
-                                            ("gloo", "compact")])
+                                            ("gloo", "compact"), ("ipc", "compact_nodes")])
 @pytest.mark.parametrize("world", [2, 3])
 def test_multiprocess_runner_on_one_gpu(world, transport, coll):
     """DistributedSlabRunner in `world` processes sharing cuda:0 == the
@@ -196,7 +209,7 @@ def test_multiprocess_runner_on_one_gpu(world, transport, coll):
         p.join(300)
         assert p.exitcode == 0
     geo = CASES["pack_io"]()
-    cfg = solver.SimulationConfig(u_max_guard=0.0, **COLLISIONS[coll])
+    cfg = solver.SimulationConfig(u_max_guard=0.0, **_split(coll)[0])
     ref = solver.Solver(geo, cfg)
     ref.set_fields_canonical(dense.to_canonical(_f0(geo, np.float64), ref.tile_grid.non_empty,
                                                 np.zeros(19)))
