@@ -440,21 +440,28 @@ def _time_solver(torch, s, steps, warmup=3):
 def porosity_block(args, torch, steps=20,
                    porosities=(0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0)):
     """BASELINE configs 3 and 4: per geometry and precision, MLUPS and
-    BU = MLUPS x B_node / peak for the paper's block storage and the compact
-    store (CUDA events over `steps` launches after 3 warm-up launches), and
-    the storage storage="auto" picks (its number is that storage's)."""
+    BU = MLUPS x B_node / peak for the paper's block storage ("blocks"), the
+    compact store with the tile-parallel step ("compact") and with the
+    node-parallel step ("nodes") -- CUDA events over `steps` launches after 3
+    warm-up launches -- and the kernel storage="auto" picks (its number is
+    that kernel's)."""
     from paper_1611_02445_b200 import workloads
     from paper_1611_02445_b200.solver import DeviceTiling, SimulationConfig, Solver
-    from paper_1611_02445_b200.solver import resolve_auto_storage
+    from paper_1611_02445_b200.solver import resolve_auto_storage, use_nodes
     peak, _ = peaks()
     cases = [(f"{p:.1f}", workloads.sphere_pack(p, n=args.edge)) for p in porosities]
     cases.append(("vessel512x512x1024", workloads.vessel_tree((512, 512, 1024))))
     out = {"workload": f"sphere pack {args.edge}^3, d=40, seed 1234 (porosity 1.0: all-fluid "
                        "box) and vessel tree 512x512x1024 (seed 1234); LBGK incompressible",
+           "kernels": {"blocks": "paper's 64-slot blocks, tile-parallel step",
+                       "compact": "compact store, tile-parallel step",
+                       "nodes": "compact store, node-parallel step"},
            "porosity": list(porosities), "eta_t": [], "vessel": {}}
+    kernels = (("blocks", "blocks", "tile"), ("compact", "compact", "tile"),
+               ("nodes", "compact", "nodes"))
+    keys = [f"{m}_{k}" for k, _, _ in kernels for m in ("mlups", "bu")]
     for prec in ("f64", "f32"):
-        out[prec] = {k: [] for k in ("mlups_blocks", "bu_blocks", "mlups_compact",
-                                     "bu_compact", "storage_auto", "mlups_auto", "bu_auto")}
+        out[prec] = {k: [] for k in keys + ["kernel_auto", "mlups_auto", "bu_auto"]}
     for name, geo in cases:
         tl = DeviceTiling(geo)
         ves = name.startswith("vessel")
@@ -466,31 +473,33 @@ def porosity_block(args, torch, steps=20,
         for prec in ("f64", "f32"):
             b_node = 2 * 19 * (8 if prec == "f64" else 4)
             rec = {}
-            for storage in ("blocks", "compact"):
+            for kname, storage, trav in kernels:
                 cfg = SimulationConfig(tau=workloads.TAU, precision=prec, u_max_guard=0.0,
                                        storage=storage)
-                s = Solver(geo, cfg, tiling=tl)
+                s = Solver(geo, cfg, tiling=tl, traversal=trav)
                 ms = _time_solver(torch, s, steps)
                 mlups = s.n_fn / (ms / 1e3) / 1e6
-                rec[storage] = (round(mlups, 1), round(mlups * 1e6 * b_node / (peak * 1e9), 4))
+                rec[kname] = (round(mlups, 1), round(mlups * 1e6 * b_node / (peak * 1e9), 4))
                 del s
                 torch.cuda.empty_cache()
-            auto = resolve_auto_storage(SimulationConfig(precision=prec, storage="auto"),
-                                        tl.n_fn, tl.t_n).storage
+            acfg = resolve_auto_storage(SimulationConfig(precision=prec, storage="auto"),
+                                        tl.n_fn, tl.t_n)
+            auto = acfg.storage
+            if auto == "compact":
+                auto = "nodes" if use_nodes(acfg, tl.n_fn, tl.t_n, "auto") else "compact"
+            d = out[prec] if not ves else out["vessel"].setdefault(prec, {})
+            for kname, _, _ in kernels:
+                for i, m in enumerate(("mlups", "bu")):
+                    if ves:
+                        d[f"{m}_{kname}"] = rec[kname][i]
+                    else:
+                        d[f"{m}_{kname}"].append(rec[kname][i])
             if ves:
-                out["vessel"][prec] = {"mlups_blocks": rec["blocks"][0],
-                                       "bu_blocks": rec["blocks"][1],
-                                       "mlups_compact": rec["compact"][0],
-                                       "bu_compact": rec["compact"][1], "storage_auto": auto,
-                                       "mlups_auto": rec[auto][0], "bu_auto": rec[auto][1]}
-                continue
-            d = out[prec]
-            for storage in ("blocks", "compact"):
-                d[f"mlups_{storage}"].append(rec[storage][0])
-                d[f"bu_{storage}"].append(rec[storage][1])
-            d["storage_auto"].append(auto)
-            d["mlups_auto"].append(rec[auto][0])
-            d["bu_auto"].append(rec[auto][1])
+                d.update(kernel_auto=auto, mlups_auto=rec[auto][0], bu_auto=rec[auto][1])
+            else:
+                d["kernel_auto"].append(auto)
+                d["mlups_auto"].append(rec[auto][0])
+                d["bu_auto"].append(rec[auto][1])
         del tl
         torch.cuda.empty_cache()
     return out

@@ -237,8 +237,9 @@ int tlbm_compact_ranks(const uint32_t *d_meta, int64_t t_n, uint8_t *d_rank, voi
  * solid slots cost no lanes).  Node n (store order: tile-major, rank-minor):
  *   d_node_meta[n] = its node word (bits 0-24) | slot << 25
  *   d_node_rec[n]  = 4 x uint32: the rank, in its source tile, of the value
- *                    it pulls in direction q = 1..18 (6 bits each, five per
- *                    word: q-1 = 5w + i at bits 6i of word w), its own rank
+ *                    it pulls in direction q = 1..18 -- its own rank where
+ *                    the link is missing (bounce-back) -- (6 bits each, five
+ *                    per word: q-1 = 5w + i at bits 6i of word w), its own rank
  *                    at bits 18-23 and its tile - d_unit_tile[n / 64] at
  *                    bits 24-29 of word 3
  *   d_unit_tile[u] = the tile of node 64u            (ceil(n_fn / 64))

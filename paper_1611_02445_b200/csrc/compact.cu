@@ -169,7 +169,10 @@ __global__ void node_records_kernel(const uint32_t *meta, const int *nbr, long l
         uint32_t w[4] = {0u, 0u, 0u, 0u};
         const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
         for (int q = 1; q < Q; ++q) {
-            if (!((m >> q) & 1u)) continue;   // bounce-back: reads its own slot
+            if (!((m >> q) & 1u)) {           // bounce-back: reads its own slot
+                w[(q - 1) / 5] |= (uint32_t)r << (6 * ((q - 1) % 5));
+                continue;
+            }
             const int sx = x - ex(q), sy = y - ey(q), sz = z - ez(q);
             const int dx = sx < 0 ? -1 : (sx > 3 ? 1 : 0);
             const int dy = sy < 0 ? -1 : (sy > 3 ? 1 : 0);

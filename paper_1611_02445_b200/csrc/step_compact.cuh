@@ -250,7 +250,8 @@ step_kernel_compact(const StepParams<T, MRT> p) {
 // (tlbm_compact_nodes): the 18 source ranks, its own rank and its tile; the
 // source tile's block offset and length come from the tile's 27-entry row of
 // {offset, count} (8-byte loads that the lanes of one tile share in L1);
-// which entry a pull reads is the compile-time pull table.  Node-level
+// which entry a pull reads follows from the slot by integer arithmetic, so
+// the gather sits three load levels deep (record -> entry -> value).  Node-level
 // metadata is 20 B + 216 B per tile (~25 B per fluid node at porosity 0.2,
 // 8% of the 304 B the populations move in fp64).
 #ifndef TLBM_NODES_THREADS
@@ -264,45 +265,73 @@ constexpr int min_blocks_nodes() {
            (TLBM_NODES_THREADS / 32);
 }
 
+// element i of base, scale = sizeof(T) passed at run time (StepParams::
+// scale_*) so the address is one IMAD.WIDE.U32 on the FMA pipe
+template <class T>
+__device__ __forceinline__ const T *at_u32(const T *base, unsigned i, unsigned scale) {
+    return reinterpret_cast<const T *>(reinterpret_cast<const char *>(base) +
+                                       (unsigned long long)i * scale);
+}
+
+// one node's gather + update; rec / meta / unit_tile already loaded
+template <class T, int QUASI, int VARIANT, bool MRT, bool FMA, bool HALO>
+__device__ __forceinline__ uint32_t node_update(const StepParams<T, MRT> &p, uint32_t meta,
+                                                uint4 rec, int unit_tile) {
+    const int j = (int)(meta >> 25);
+    const int rank_own = (int)((rec.w >> 18) & 63u);
+    const long long tile = (long long)unit_tile + ((rec.w >> 24) & 63u);
+    const uint2 *ent = reinterpret_cast<const uint2 *>(p.entries) + tile * NBR;
+    const uint2 mine = __ldg(ent + 13);
+    const unsigned own = mine.x;
+    const int nf_own = (int)mine.y;
+    const T *base0 = p.src;
+    // neighbour-row entry of each pull without a table load: a pull in
+    // direction e crosses into the tile at -e on the axes where the slot
+    // sits on the face it pulls across; the entry index is 13 plus the
+    // crossing axes' contributions (9, 3, 1 per tile step in x, y, z)
+    const int x = j & 3, y = (j >> 2) & 3, z = j >> 4;
+    const int cx[2] = {x == 0 ? -9 : 0, x == 3 ? 9 : 0};   // e_x = +1, -1
+    const int cy[2] = {y == 0 ? -3 : 0, y == 3 ? 3 : 0};
+    const int cz[2] = {z == 0 ? -1 : 0, z == 3 ? 1 : 0};
+    const unsigned own_r = own + (unsigned)rank_own;
+    T g[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
+            g[q] = load_ro(at_u32(base0, own + (unsigned)(q * nf_own + rank_own), p.scale_value));
+            continue;
+        }
+        // the record holds the source rank (the node's own rank where there
+        // is no link; halfway bounce-back reads block opp(q) of its own tile)
+        const uint32_t word = (q - 1) < 5 ? rec.x : (q - 1) < 10 ? rec.y
+                            : (q - 1) < 15 ? rec.z : rec.w;
+        const int r = (int)((word >> (6 * ((q - 1) % 5))) & 63u);
+        // the entry of the pull's source tile is read whether or not the
+        // link exists (every entry is valid: a missing neighbour is the tile
+        // itself), so only the final offset is selected
+        const bool link = (meta >> q) & 1u;
+        const int kq = 13 + (ex(q) > 0 ? cx[0] : ex(q) < 0 ? cx[1] : 0) +
+                       (ey(q) > 0 ? cy[0] : ey(q) < 0 ? cy[1] : 0) +
+                       (ez(q) > 0 ? cz[0] : ez(q) < 0 ? cz[1] : 0);
+        const uint2 e = __ldg(at_u32(ent, (unsigned)kq, p.scale_entry));
+        const unsigned pulled = e.x + (unsigned)(q * (int)e.y + r);
+        const unsigned bounced = own_r + (unsigned)(opp(q) * nf_own);
+        g[q] = load_ro(at_u32(base0, link ? pulled : bounced, p.scale_value));
+    }
+    return compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, tile, j, meta, g, own, nf_own,
+                                                             rank_own);
+}
+
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA, bool HALO>
 __global__ void __launch_bounds__(TLBM_NODES_THREADS, min_blocks_nodes<T, MRT, FMA>())
 step_kernel_nodes(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
-    const long long n = p.node_begin + (long long)blockIdx.x * TLBM_NODES_THREADS + threadIdx.x;
     uint32_t status = 0;
-    if (n < p.node_end) {
-        const uint32_t meta = __ldg(p.node_meta + n);
-        const uint4 rec = __ldg(reinterpret_cast<const uint4 *>(p.node_rec) + n);
-        const int j = (int)(meta >> 25);
-        const int rank_own = (int)((rec.w >> 18) & 63u);
-        const long long tile = (long long)__ldg(p.unit_tile + (n >> 6)) + ((rec.w >> 24) & 63u);
-        const uint2 *ent = reinterpret_cast<const uint2 *>(p.entries) + tile * NBR;
-        const uint2 mine = __ldg(ent + 13);
-        const unsigned own = mine.x;
-        const int nf_own = (int)mine.y;
-        const T *base0 = opaque(p.src);
-        T g[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
-                g[q] = load_ro(base0 + (own + (unsigned)(q * nf_own + rank_own)));
-                continue;
-            }
-            const uint32_t word = (q - 1) < 5 ? rec.x : (q - 1) < 10 ? rec.y
-                                : (q - 1) < 15 ? rec.z : rec.w;
-            const int rs = (int)((word >> (6 * ((q - 1) % 5))) & 63u);
-            // no link: halfway bounce-back reads the node's own slot of
-            // block opp(q) (entry 13 is the own tile)
-            const bool link = (meta >> q) & 1u;
-            const int k = link ? (int)(__ldg(&kCompactPull.w[q * 64 + j]) >> 6) : 13;
-            const uint2 e = __ldg(ent + k);
-            const int blk = link ? q : opp(q);
-            const int r = link ? rs : rank_own;
-            g[q] = load_ro(base0 + (e.x + (unsigned)(blk * (int)e.y + r)));
-        }
-        status = compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, tile, j, meta, g, own,
-                                                                   nf_own, rank_own);
-    }
+    const long long n = p.node_begin + (long long)blockIdx.x * TLBM_NODES_THREADS + threadIdx.x;
+    if (n < p.node_end)
+        status = node_update<T, QUASI, VARIANT, MRT, FMA, HALO>(
+            p, __ldg(p.node_meta + n), __ldg(reinterpret_cast<const uint4 *>(p.node_rec) + n),
+            __ldg(p.unit_tile + (n >> 6)));
     report_status(p, status);
 }
 

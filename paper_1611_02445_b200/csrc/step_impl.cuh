@@ -71,6 +71,10 @@ struct StepParams {
     const int *__restrict__ unit_tile;
     const void *__restrict__ entries;
     long long node_begin, node_end;
+    // sizeof(T) and sizeof(uint2) as run-time values: ptxas cannot
+    // strength-reduce base + i * scale into a LEA / LEA.HI.X pair (ALU pipe)
+    // and keeps one IMAD.WIDE.U32 (FMA pipe) per address (step_kernel_nodes)
+    unsigned scale_value, scale_entry;
 };
 
 // the tile at launch position pos (tile_begin <= pos < tile_end); ORDERED
@@ -609,6 +613,8 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     p.entries = a->entries;
     p.node_begin = a->node_begin;
     p.node_end = a->node_end;
+    p.scale_value = sizeof(T);
+    p.scale_entry = sizeof(uint2);
 }
 
 template <class T>

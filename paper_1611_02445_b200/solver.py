@@ -14,8 +14,9 @@ step semantics are restated in SURVEY Appendix A).  API:
                       "blocks" (default, the paper's 64-slot blocks) or
                       "compact" (only the non-solid slots of every block;
                       less DRAM traffic on sparse geometries)
-                      or "auto" (compact for fp64 when the tile
-                      utilisation eta_t < AUTO_COMPACT_ETA, else blocks).
+                      or "auto" (compact, with the node-parallel step, when
+                      the tile utilisation eta_t < AUTO_COMPACT_ETA of the
+                      precision, else blocks).
 ``SimulationState``   SPEC.md:341-345 (geometry, tile grid, field store,
                       iteration, parity).
 ``Solver``            owns the device state; ``step(n)``, ``run(n)``,
@@ -595,8 +596,11 @@ def traversal_order(tiling, store, traversal="auto"):
 
 
 # traversal="auto" on compact storage: the node-parallel step below this
-# tile utilisation (placeholder until measured)
-AUTO_NODES_ETA = 0.0
+# tile utilisation.  From the porosity sweep (profiles/r2_nodes_sweep.jsonl):
+# nodes beats the tile-parallel compact kernel at every porosity up to 0.8
+# (fp64 0.873 vs 0.743 BU at porosity 0.2, fp32 0.708 vs 0.535) and trails
+# it slightly on near-full tiles (fp64 0.884 vs 0.899 at eta_t 0.97).
+AUTO_NODES_ETA = 0.95
 
 
 def use_nodes(config, n_fn, t_n, traversal):
@@ -610,17 +614,19 @@ def use_nodes(config, n_fn, t_n, traversal):
     return n_fn / (64.0 * t_n) < AUTO_NODES_ETA
 
 
-# storage="auto": compact below this tile utilisation (fp64).  From the
-# porosity sweep (profiles/r1b_porosity_sweep_storage.jsonl): compact is
-# +2% at eta_t 0.866 (porosity 0.6), -1.5% at 0.904 (0.7), +21% at 0.658.
-AUTO_COMPACT_ETA = 0.88
+# storage="auto": compact storage (with the node-parallel step) below this
+# tile utilisation, per precision.  From the porosity sweep
+# (profiles/r2_nodes_sweep.jsonl), nodes vs the paper's blocks: fp64 +41% at
+# eta_t 0.658 (porosity 0.2), +13% at 0.825 (0.5), tie at 0.904 (0.7),
+# -9% at 0.971 (0.9); fp32 +30% at 0.658, tie at 0.825, -10% at 0.904.
+AUTO_COMPACT_ETA = {"f64": 0.90, "f32": 0.80}
 
 
 def resolve_auto_storage(config, n_fn, t_n):
     """The concrete configuration storage="auto" stands for on a tiling."""
     import dataclasses
     eta = n_fn / (64.0 * t_n) if t_n else 1.0
-    compact = config.precision == "f64" and eta < AUTO_COMPACT_ETA
+    compact = eta < AUTO_COMPACT_ETA[config.precision]
     return dataclasses.replace(config, storage="compact" if compact else "blocks", table=None)
 
 

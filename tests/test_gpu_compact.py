@@ -128,8 +128,15 @@ def test_auto_storage_picks_by_tile_utilisation():
     sparse = geometry.generate_sphere_pack(32, 8, 0.3, seed=1, inlet_velocity=(0, 0, 0.01))
     dense = geometry.generate_channel("square", 16, axis=2, length=16, ends="periodic")
     cfg = solver.SimulationConfig(storage="auto", u_max_guard=0.0)
-    assert solver.Solver(sparse, cfg).config.storage == "compact"
+    s = solver.Solver(sparse, cfg)
+    assert s.config.storage == "compact" and s.nodes is not None     # node-parallel step
     assert solver.Solver(dense, cfg).config.storage == "blocks"
+    # fp32: compact below eta_t 0.80 only
+    eta = sparse_eta = s.n_fn / (64 * s.t_n)
+    want = "compact" if eta < solver.AUTO_COMPACT_ETA["f32"] else "blocks"
+    cfg32 = solver.SimulationConfig(storage="auto", u_max_guard=0.0, precision="f32")
+    assert solver.Solver(sparse, cfg32).config.storage == want, sparse_eta
+    assert solver.Solver(sparse, cfg, traversal="tile").nodes is None
 
 
 def test_node_records_decode():
@@ -169,7 +176,8 @@ def test_node_records_decode():
             assert rec["unit_tile"][n >> 6] + ((w[3] >> 24) & 63) == t
             x, y, z = j & 3, (j >> 2) & 3, j >> 4
             for q in range(1, 19):
-                if not (m >> q) & 1:
+                if not (m >> q) & 1:      # bounce-back: the node's own rank
+                    assert (w[(q - 1) // 5] >> (6 * ((q - 1) % 5))) & 63 == r
                     continue
                 sx, sy, sz = x - e[q][0], y - e[q][1], z - e[q][2]
                 d = [(-1 if v < 0 else (1 if v > 3 else 0)) for v in (sx, sy, sz)]

@@ -130,9 +130,17 @@ def test_auto_storage_resolution():
     dense = solver.resolve_auto_storage(c, n_fn=64 * 100, t_n=100)
     assert (sparse.storage, sparse.table) == ("compact", layout.LayoutTable.XYZ)
     assert (dense.storage, dense.table) == ("blocks", layout.LayoutTable.B200)
-    f32 = solver.resolve_auto_storage(solver.SimulationConfig(storage="auto", precision="f32"),
-                                      n_fn=40 * 100, t_n=100)
-    assert f32.storage == "blocks"
+    f32 = lambda n: solver.resolve_auto_storage(        # noqa: E731
+        solver.SimulationConfig(storage="auto", precision="f32"), n_fn=n, t_n=100)
+    assert f32(40 * 100).storage == "compact"                           # eta_t 0.625
+    assert f32(54 * 100).storage == "blocks"                            # eta_t 0.84
+    assert solver.resolve_auto_storage(c, n_fn=54 * 100, t_n=100).storage == "compact"
+    # compact storage runs the node-parallel step below AUTO_NODES_ETA
+    assert solver.use_nodes(sparse, 40 * 100, 100, "auto")
+    assert not solver.use_nodes(sparse, 40 * 100, 100, "tile")
+    assert not solver.use_nodes(dense, 64 * 100, 100, "auto")
+    with pytest.raises(ValueError):
+        solver.use_nodes(dense, 64 * 100, 100, "nodes")
     with pytest.raises(ValueError):
         solver.SimulationConfig(storage="auto", table="xyz")
 
