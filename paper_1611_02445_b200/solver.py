@@ -596,10 +596,10 @@ def traversal_order(tiling, store, traversal="auto"):
 
 
 # traversal="auto" on compact storage: the node-parallel step below this
-# tile utilisation.  From the porosity sweep (profiles/r2_nodes_sweep.jsonl):
+# tile utilisation.  From the bench porosity block (profiles/r2b_bench_n1.json):
 # nodes beats the tile-parallel compact kernel at every porosity up to 0.8
-# (fp64 0.873 vs 0.743 BU at porosity 0.2, fp32 0.708 vs 0.535) and trails
-# it slightly on near-full tiles (fp64 0.884 vs 0.899 at eta_t 0.97).
+# (fp64 0.879 vs 0.749 BU at porosity 0.2, fp32 0.714 vs 0.538) and trails
+# it slightly on near-full tiles (fp64 0.886 vs 0.895 at eta_t 0.971).
 AUTO_NODES_ETA = 0.95
 
 
@@ -615,11 +615,12 @@ def use_nodes(config, n_fn, t_n, traversal):
 
 
 # storage="auto": compact storage (with the node-parallel step) below this
-# tile utilisation, per precision.  From the porosity sweep
-# (profiles/r2_nodes_sweep.jsonl), nodes vs the paper's blocks: fp64 +41% at
-# eta_t 0.658 (porosity 0.2), +13% at 0.825 (0.5), tie at 0.904 (0.7),
-# -9% at 0.971 (0.9); fp32 +30% at 0.658, tie at 0.825, -10% at 0.904.
-AUTO_COMPACT_ETA = {"f64": 0.90, "f32": 0.80}
+# tile utilisation, per precision.  From the bench porosity block
+# (profiles/r2b_bench_n1.json), nodes vs the paper's blocks: fp64 +42% at
+# eta_t 0.658 (porosity 0.2), +7% at 0.866 (0.6), +0.5% at 0.904 (0.7), +2%
+# on the vessel tree (0.927), -5% at 0.939 (0.8); fp32 +31% at 0.658, tie
+# at 0.825 (0.5), -5% at 0.866.
+AUTO_COMPACT_ETA = {"f64": 0.93, "f32": 0.83}
 
 
 def resolve_auto_storage(config, n_fn, t_n):

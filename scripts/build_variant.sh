@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build an experimental libtlbm.so with extra -D flags on the step kernels:
-#   scripts/build_variant.sh NAME "-DTLBM_MINB=12 -DTLBM_PULL_MODE=2"
+#   [ONLY=f32|f64] scripts/build_variant.sh NAME "-DTLBM_MINB=12 -DTLBM_PULL_MODE=2"
 # -> build/variants/NAME/libtlbm.so (select it with TLBM_LIB=...; used by
 # scripts/step_sweep.py tuning runs).  The main objects come from `make`.
 set -eu
@@ -11,10 +11,16 @@ mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 NV="nvcc -O3 -std=c++20 $ARCH -lineinfo -fmad=false -Xptxas -v -Xcompiler -fPIC -I$ROOT/include --expt-relaxed-constexpr $FLAGS"
 C=$ROOT/paper_1611_02445_b200/csrc
-$NV -c -o $OUT/step_f32.o $C/step_f32.cu 2> $OUT/f32.log &
-$NV -c -o $OUT/step_f64.o $C/step_f64.cu 2> $OUT/f64.log &
-wait
+# ONLY=f32 / ONLY=f64 rebuilds one dtype and links the main build's other one
 O=$ROOT/paper_1611_02445_b200/lib/obj
+for d in f32 f64; do
+  if [ -z "${ONLY:-}" ] || [ "${ONLY:-}" = $d ]; then
+    $NV -c -o $OUT/step_$d.o $C/step_$d.cu 2> $OUT/$d.log &
+  else
+    cp $O/step_$d.o $OUT/step_$d.o
+  fi
+done
+wait
 nvcc $ARCH -shared -o $OUT/libtlbm.so $(ls $O/*.o | grep -v -E "step_f(32|64).o") \
     $OUT/step_f32.o $OUT/step_f64.o
 echo $OUT/libtlbm.so

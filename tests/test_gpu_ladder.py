@@ -17,7 +17,11 @@ TIE = 0.03
 
 
 def _mflups(s, variant, blocks=8):
-    s.step(solver.GRAPH_STEPS, variant=variant, graph=True)    # capture + warm up
+    # every rung from the cold start (the bench variants are not physical
+    # steps: their state is not a valid start for the next rung); the status
+    # words are not read
+    s.init_equilibrium()
+    s.step(solver.GRAPH_STEPS, variant=variant, graph=True, check=False)   # capture + warm up
     torch.cuda.synchronize()
     best = float("inf")
     for _ in range(3):
@@ -27,7 +31,6 @@ def _mflups(s, variant, blocks=8):
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 1e3 / (blocks * solver.GRAPH_STEPS))
-    s.check()
     return s.n_fn / best / 1e6
 
 
@@ -48,4 +51,6 @@ def test_ladder_ordering_cavity100(precision):
     # utilisation as the paper computes it: MFLUPS * B_node / bandwidth
     b_node = txmodel.b_node(19, 8 if precision == "f64" else 4)
     assert b_node == (304 if precision == "f64" else 152)
+    lbgk.init_equilibrium()
+    lbgk.step(200)                               # the physical rung stays finite
     assert np.isfinite(lbgk.fields_canonical()).all()

