@@ -75,6 +75,14 @@ constexpr int min_blocks_compact() {
            (2 * compact_tiles_per_cta<T>());
 }
 
+// element i of base, scale = sizeof(T) passed at run time (StepParams::
+// scale_*) so the address is one IMAD.WIDE.U32 on the FMA pipe
+template <class T>
+__device__ __forceinline__ T *at_u32(T *base, unsigned i, unsigned scale) {
+    using B = std::conditional_t<std::is_const_v<T>, const char, char>;
+    return reinterpret_cast<T *>(reinterpret_cast<B *>(base) + (unsigned long long)i * scale);
+}
+
 // The tail of a node's update on the compact store, shared by the compact
 // kernels: boundary handling, collision, the store into the other copy at
 // own + q * nf_own + rank_own, and the fused halo.
@@ -102,9 +110,17 @@ __device__ __forceinline__ uint32_t compact_finish(const StepParams<T, MRT> &p, 
                 status = collide<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
         }
     }
-    T *out = p.dst + own;
+    if constexpr (std::is_same_v<Off, unsigned>) {
+        // 32-bit offsets: one IMAD + one IMAD.WIDE per store
+        T *out = at_u32(p.dst, own + (unsigned)rank_own, p.scale_value);
 #pragma unroll
-    for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
+        for (int q = 0; q < Q; ++q)
+            store_out(at_u32(out, (unsigned)(q * nf_own), p.scale_value), g[q]);
+    } else {
+        T *out = p.dst + own;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) store_out(out + (q * nf_own + rank_own), g[q]);
+    }
     if constexpr (HALO) {
         // fused halo: the neighbour's ghost copy of this tile has the same
         // nodes (same ranks and count), at its own block offset
@@ -263,14 +279,6 @@ constexpr int min_blocks_nodes() {
                                   : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
                 : (sizeof(T) == 4 ? TLBM_WARPS_NODES_F32 : TLBM_WARPS_COMPACT)) /
            (TLBM_NODES_THREADS / 32);
-}
-
-// element i of base, scale = sizeof(T) passed at run time (StepParams::
-// scale_*) so the address is one IMAD.WIDE.U32 on the FMA pipe
-template <class T>
-__device__ __forceinline__ const T *at_u32(const T *base, unsigned i, unsigned scale) {
-    return reinterpret_cast<const T *>(reinterpret_cast<const char *>(base) +
-                                       (unsigned long long)i * scale);
 }
 
 // one node's gather + update; rec / meta / unit_tile already loaded
