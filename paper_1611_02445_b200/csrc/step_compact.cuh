@@ -39,7 +39,7 @@ namespace step_detail {
 #define TLBM_WARPS_COMPACT_F32 48
 #endif
 #ifndef TLBM_WARPS_NODES_F32
-#define TLBM_WARPS_NODES_F32 48
+#define TLBM_WARPS_NODES_F32 (TLBM_NODES_NPT_F32 == 1 ? 48 : TLBM_NODES_NPT_F32 == 2 ? 32 : 24)
 #endif
 // per (q, j): 64 * (neighbour-row entry of the source tile) + source slot
 struct CompactPull {
@@ -273,18 +273,42 @@ step_kernel_compact(const StepParams<T, MRT> p) {
 #ifndef TLBM_NODES_THREADS
 #define TLBM_NODES_THREADS 128
 #endif
+// nodes per thread of the fp32 LBGK node-parallel step: two, at 32 warps/SM
+// (64 registers), beat one at 48 warps/SM by 2-3% below porosity 0.6
+// (scripts/exp/exp50.sh)
+#ifndef TLBM_NODES_NPT_F32
+#define TLBM_NODES_NPT_F32 2
+#endif
+#ifndef TLBM_NODES_NPT_F64
+#define TLBM_NODES_NPT_F64 1
+#endif
+#ifndef TLBM_WARPS_NODES_F64
+#define TLBM_WARPS_NODES_F64 (TLBM_NODES_NPT_F64 == 1 ? TLBM_WARPS_COMPACT : 16)
+#endif
+template <class T, bool MRT>
+constexpr int nodes_per_thread() {
+    return MRT ? 1 : (sizeof(T) == 4 ? TLBM_NODES_NPT_F32 : TLBM_NODES_NPT_F64);
+}
 template <class T, bool MRT, bool FMA = false>
 constexpr int min_blocks_nodes() {
     return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32
                                   : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
-                : (sizeof(T) == 4 ? TLBM_WARPS_NODES_F32 : TLBM_WARPS_COMPACT)) /
+                : (sizeof(T) == 4 ? TLBM_WARPS_NODES_F32 : TLBM_WARPS_NODES_F64)) /
            (TLBM_NODES_THREADS / 32);
 }
 
-// one node's gather + update; rec / meta / unit_tile already loaded
-template <class T, int QUASI, int VARIANT, bool MRT, bool FMA, bool HALO>
-__device__ __forceinline__ uint32_t node_update(const StepParams<T, MRT> &p, uint32_t meta,
-                                                uint4 rec, int unit_tile) {
+// what the tail of a node's update needs besides its gathered values
+struct NodeCtx {
+    long long tile;
+    uint32_t meta;
+    unsigned own;
+    int nf_own, rank_own;
+};
+
+// one node's gather; rec / meta / unit_tile already loaded
+template <class T, int VARIANT, bool MRT>
+__device__ __forceinline__ NodeCtx node_gather(const StepParams<T, MRT> &p, uint32_t meta,
+                                               uint4 rec, int unit_tile, T (&g)[Q]) {
     const int j = (int)(meta >> 25);
     const int rank_own = (int)((rec.w >> 18) & 63u);
     const long long tile = (long long)unit_tile + ((rec.w >> 24) & 63u);
@@ -302,7 +326,6 @@ __device__ __forceinline__ uint32_t node_update(const StepParams<T, MRT> &p, uin
     const int cy[2] = {y == 0 ? -3 : 0, y == 3 ? 3 : 0};
     const int cz[2] = {z == 0 ? -1 : 0, z == 3 ? 1 : 0};
     const unsigned own_r = own + (unsigned)rank_own;
-    T g[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         if (VARIANT == TLBM_READ_WRITE_ONLY || q == 0) {
@@ -326,20 +349,57 @@ __device__ __forceinline__ uint32_t node_update(const StepParams<T, MRT> &p, uin
         const unsigned bounced = own_r + (unsigned)(opp(q) * nf_own);
         g[q] = load_ro(at_u32(base0, link ? pulled : bounced, p.scale_value));
     }
-    return compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, tile, j, meta, g, own, nf_own,
-                                                             rank_own);
+    return NodeCtx{tile, meta, own, nf_own, rank_own};
+}
+
+template <class T, int QUASI, int VARIANT, bool MRT, bool FMA, bool HALO>
+__device__ __forceinline__ uint32_t node_finish(const StepParams<T, MRT> &p, const NodeCtx &c,
+                                                T (&g)[Q]) {
+    return compact_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(
+        p, c.tile, (int)(c.meta >> 25), c.meta, g, c.own, c.nf_own, c.rank_own);
+}
+
+template <class T, int VARIANT, bool MRT>
+__device__ __forceinline__ NodeCtx node_load_gather(const StepParams<T, MRT> &p, long long n,
+                                                    T (&g)[Q]) {
+    return node_gather<T, VARIANT, MRT>(
+        p, __ldg(p.node_meta + n), __ldg(reinterpret_cast<const uint4 *>(p.node_rec) + n),
+        __ldg(p.unit_tile + (n >> 6)), g);
 }
 
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA, bool HALO>
 __global__ void __launch_bounds__(TLBM_NODES_THREADS, min_blocks_nodes<T, MRT, FMA>())
 step_kernel_nodes(const StepParams<T, MRT> p) {
     static_assert(compact_table_ok(TABLE), "compact storage keeps blocks in XYZ order");
+    constexpr int NPT = nodes_per_thread<T, MRT>();
     uint32_t status = 0;
-    const long long n = p.node_begin + (long long)blockIdx.x * TLBM_NODES_THREADS + threadIdx.x;
-    if (n < p.node_end)
-        status = node_update<T, QUASI, VARIANT, MRT, FMA, HALO>(
-            p, __ldg(p.node_meta + n), __ldg(reinterpret_cast<const uint4 *>(p.node_rec) + n),
-            __ldg(p.unit_tile + (n >> 6)));
+    const long long n = p.node_begin + (long long)blockIdx.x * TLBM_NODES_THREADS * NPT +
+                        threadIdx.x;
+    if constexpr (NPT == 1) {
+        if (n < p.node_end) {
+            T g[Q];
+            const NodeCtx c = node_load_gather<T, VARIANT, MRT>(p, n, g);
+            status = node_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, c, g);
+        }
+    } else {
+        // NPT nodes per thread, CTA-strided: every gather in flight before
+        // the first update (a node past the end gathers the last node again
+        // and is not stored)
+        if (n < p.node_end) {
+            T g[NPT][Q];
+            NodeCtx c[NPT];
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                const long long nk = n + (long long)k * TLBM_NODES_THREADS;
+                c[k] = node_load_gather<T, VARIANT, MRT>(p, nk < p.node_end ? nk : p.node_end - 1,
+                                                         g[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < NPT; ++k)
+                if (k == 0 || n + (long long)k * TLBM_NODES_THREADS < p.node_end)
+                    status |= node_finish<T, QUASI, VARIANT, MRT, FMA, HALO>(p, c[k], g[k]);
+        }
+    }
     report_status(p, status);
 }
 

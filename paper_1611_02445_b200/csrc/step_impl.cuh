@@ -435,7 +435,8 @@ int launch_nodes(const tlbm_step_args *a, cudaStream_t s) {
     fill_params<T, MRT, FMA>(p, a);
     const long long n = a->node_end - a->node_begin;
     if (n <= 0) return TLBM_OK;
-    const unsigned grid = (unsigned)((n + TLBM_NODES_THREADS - 1) / TLBM_NODES_THREADS);
+    constexpr int per_cta = TLBM_NODES_THREADS * nodes_per_thread<T, MRT>();
+    const unsigned grid = (unsigned)((n + per_cta - 1) / per_cta);
     if (VARIANT == TLBM_FULL && (a->halo_up || a->halo_down))
         step_kernel_nodes<T, QUASI, TABLE, VARIANT, MRT, FMA, VARIANT == TLBM_FULL>
             <<<grid, TLBM_NODES_THREADS, 0, s>>>(p);
