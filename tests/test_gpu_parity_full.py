@@ -154,14 +154,17 @@ def test_step_channel_256(c_oracle, prec, arith):
     print(f"channel256 {prec} {arith}: rel f/rho/u = {r}")
 
 
-@pytest.mark.parametrize("storage", ["blocks", "compact"])
+@pytest.mark.parametrize("storage,traversal", [("blocks", "tile"), ("compact", "tile"),
+                                               ("compact", "nodes")])
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-def test_step_sphere_pack_256_p02(c_oracle, prec, storage):
+def test_step_sphere_pack_256_p02(c_oracle, prec, storage, traversal):
     """BASELINE config 3 at porosity 0.2 (tile utilisation 0.66), inlet z = 0 /
-    outlet z = 255, both storages, 10 steps from a perturbed start."""
+    outlet z = 255, both storages and both compact kernels (tile- and
+    node-parallel), 10 steps from a perturbed start."""
     geo = workloads.sphere_pack(0.2)
-    s = workloads.make_solver(geo, prec, u0=(0.0, 0.0, 0.01), storage=storage)
-    assert s.config.storage == storage
+    s = workloads.make_solver(geo, prec, u0=(0.0, 0.0, 0.01), storage=storage,
+                              traversal=traversal)
+    assert s.config.storage == storage and (s.nodes is not None) == (traversal == "nodes")
     _step_parity(c_oracle, s, geo)
 
 
@@ -172,6 +175,7 @@ def test_step_sphere_pack_256_p05_quasi_mrt(c_oracle):
     cfg = SimulationConfig(collision="mrt", fluid="quasi-compressible", tau=workloads.TAU,
                            precision="f64", storage="compact")
     s = Solver(geo, cfg)
+    assert s.nodes is not None          # eta_t 0.825: the node-parallel step
     rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.01))
     s.init_from_macroscopic(rho, u)
     _step_parity(c_oracle, s, geo)

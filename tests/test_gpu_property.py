@@ -1,7 +1,8 @@
 """GPU property test (SPEC acceptance 6, hypothesis-driven): on random
 geometries -- shape, solid fraction, bounce-back / inlet / outlet faces,
 periodic axes -- and random solver configurations (dtype, fluid model,
-layout table, storage, collision model, arithmetic, CUDA-graph replay), the
+layout table, storage -- blocks, or compact with the tile- or node-parallel
+step -- collision model, arithmetic, CUDA-graph replay), the
 fused step equals the CPU oracle bit-exactly (reference arithmetic) or
 within the stated tolerance (FMA arithmetic)."""
 
@@ -27,7 +28,7 @@ def cases(draw):
     seed = draw(st.integers(0, 2 ** 31 - 1))
     prec = draw(st.sampled_from(["f64", "f32"]))
     fluid = draw(st.sampled_from(["incompressible", "quasi-compressible"]))
-    storage = draw(st.sampled_from(["blocks", "compact"]))
+    storage = draw(st.sampled_from(["blocks", "compact", "compact-nodes"]))
     table = draw(st.sampled_from(["b200", "optimized", "xyz"])) if storage == "blocks" else "xyz"
     coll = draw(st.sampled_from(["lbgk", "mrt"]))
     arith = draw(st.sampled_from(["reference", "fma"])) if prec == "f64" else "reference"
@@ -50,13 +51,14 @@ def test_step_matches_oracle(c_oracle, case):
                             periodic=per)
     dt = np.float64 if prec == "f64" else np.float32
     op = solver.SimulationConfig(collision="mrt").mrt_operator if coll == "mrt" else None
+    traversal = "nodes" if storage == "compact-nodes" else "tile"
     cfg = solver.SimulationConfig(collision=coll, fluid=fluid, tau=0.6, precision=prec,
-                                  table=table, storage=storage, arithmetic=arith,
+                                  table=table, storage=storage.split("-")[0], arithmetic=arith,
                                   u_max_guard=0.0, mrt_matrix=op)
     m = cfg.fluid
     f0 = perturbed_eq(shape, m, dt, (0.0, 0.0, 0.01), seed % 1000)
     want = oracle_run(c_oracle, geo, m, dt, f0, steps, mrt_operator=op)
-    s = solver.Solver(geo, cfg)
+    s = solver.Solver(geo, cfg, traversal=traversal)
     s.set_fields_canonical(dense.to_canonical(f0, s.tile_grid.non_empty, nm.W))
     if graph:
         solver.GRAPH_STEPS, saved = 2, solver.GRAPH_STEPS   # small graphs: exercise replay
