@@ -345,6 +345,32 @@ __device__ __forceinline__ uint32_t mrt_deviations(const T (&g)[Q], T (&d)[Q], T
 // equals the dense product bit for bit (up to the sign of an all-zero row
 // sum: the first term starts the row instead of 0 + term).  209 instead of
 // 361 multiplies, and 19 independent row chains.
+// fp32 grouped products in pairs: one packed FMUL2 (sm_100a mul.rn.f32x2,
+// IEEE round-to-nearest per lane, so bit-identical to two FMULs) for two
+// distinct values of a column; the row sums stay scalar FADDs, which ptxas
+// does not contract with a packed product.  Columns start at even offsets
+// of the operator table (mrt_offset_even) so each pair is one 8-byte load.
+#ifndef TLBM_MRT_PACKED
+#define TLBM_MRT_PACKED 1
+#endif
+__host__ __device__ constexpr int mrt_offset_even(int j) {
+    int o = 0;
+    for (int c = 0; c < j; ++c) o += (mrt_count(c) + 1) & ~1;
+    return o;
+}
+// where column j's distinct values start in the kernel's operator table
+template <class T>
+__host__ __device__ constexpr int mrt_table_offset(int j) {
+    return (sizeof(T) == 4 && TLBM_MRT_PACKED) ? mrt_offset_even(j) : mrt_offset(j);
+}
+__device__ __forceinline__ void mul2_bcast(const float *c, float d, float &r0, float &r1) {
+    unsigned long long cc, dd, rr;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c[0]), "f"(c[1]));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(dd) : "f"(d));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(rr) : "l"(cc), "l"(dd));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rr));
+}
+
 template <class T, int QUASI>
 __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq,
                                                 bool grouped = false) {
@@ -355,9 +381,22 @@ __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
             T prod[kMrtMaxPerColumn];
+            constexpr bool kPacked = sizeof(T) == 4 && TLBM_MRT_PACKED;
+            const int o = mrt_table_offset<T>(j);
 #pragma unroll
-            for (int k = 0; k < kMrtMaxPerColumn; ++k)
-                if (k < mrt_count(j)) prod[k] = op[mrt_offset(j) + k] * d[j];
+            for (int k = 0; k < kMrtMaxPerColumn; ++k) {
+                if (k >= mrt_count(j)) continue;
+                if constexpr (kPacked) {
+                    if (k & 1) continue;
+                    if (k + 1 < mrt_count(j)) {
+                        mul2_bcast(reinterpret_cast<const float *>(op + o + k), float(d[j]),
+                                   reinterpret_cast<float &>(prod[k]),
+                                   reinterpret_cast<float &>(prod[k + 1]));
+                        continue;
+                    }
+                }
+                prod[k] = op[o + k] * d[j];
+            }
 #pragma unroll
             for (int i = 0; i < Q; ++i)
                 acc[i] = j == 0 ? prod[mrt_group(i, j)] : acc[i] + prod[mrt_group(i, j)];

@@ -579,7 +579,8 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
         else if (grouped)
             for (int j = 0; j < Q; ++j)
                 for (int k = 0; k < mrt_count(j); ++k)
-                    p.mrt.op[mrt_offset(j) + k] = T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]);
+                    p.mrt.op[mrt_table_offset<T>(j) + k] =
+                        T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]);
         else
             for (int k = 0; k < Q * Q; ++k) p.mrt.op[k] = T(a->mrt_op[k]);
     }
