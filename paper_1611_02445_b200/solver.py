@@ -611,7 +611,8 @@ def use_nodes(config, n_fn, t_n, traversal):
         return True
     if traversal != "auto" or config.storage != "compact" or not t_n:
         return False
-    return n_fn / (64.0 * t_n) < AUTO_NODES_ETA
+    # the node-parallel step addresses a copy with 32-bit offsets
+    return n_fn / (64.0 * t_n) < AUTO_NODES_ETA and Q * n_fn < 2 ** 32
 
 
 # storage="auto": compact storage (with the node-parallel step) below this

@@ -139,6 +139,8 @@ def test_auto_storage_resolution():
     assert solver.use_nodes(sparse, 40 * 100, 100, "auto")
     assert not solver.use_nodes(sparse, 40 * 100, 100, "tile")
     assert not solver.use_nodes(dense, 64 * 100, 100, "auto")
+    big = 2 ** 32 // 19 + 1                   # 32-bit offsets no longer reach
+    assert not solver.use_nodes(sparse, big, big // 40 + 1, "auto")
     with pytest.raises(ValueError):
         solver.use_nodes(dense, 64 * 100, 100, "nodes")
     with pytest.raises(ValueError):
