@@ -30,19 +30,26 @@ for coll in ("lbgk", "mrt"):
     s.step(2)
 chan = geometry.generate_channel("square", 12, axis=2, length=24, ends="periodic")
 for fused in (False, True):
-    for storage in ("blocks", "compact"):
-        vs = slabs.VirtualSlabs(chan, 3, solver.SimulationConfig(storage=storage), fused=fused)
+    for storage, trav in (("blocks", "tile"), ("compact", "tile"), ("compact", "nodes")):
+        vs = slabs.VirtualSlabs(chan, 3, solver.SimulationConfig(storage=storage), fused=fused,
+                                traversal=trav)
         vs.step(3)
 for prec in ("f64", "f32"):
-    s = solver.Solver(geo, solver.SimulationConfig(precision=prec, storage="compact"))
+    for trav in ("tile", "nodes"):        # tile- and node-parallel compact steps
+        s = solver.Solver(geo, solver.SimulationConfig(precision=prec, storage="compact"),
+                          traversal=trav)
+        s.step(2)
+        s.step(1, variant=nat.PROPAGATION_ONLY)
+        s.step(1, variant=nat.READ_WRITE_ONLY)
+        s.macroscopic()
+        s.fields_canonical()
+        s = solver.Solver(geo, solver.SimulationConfig(precision=prec, storage="compact",
+                                                       collision="mrt"), traversal=trav)
+        s.step(2)
+for trav in ("tile", "nodes"):
+    s = solver.Solver(geo, solver.SimulationConfig(collision="mrt", storage="compact",
+                                                   arithmetic="fma"), traversal=trav)
     s.step(2)
-    s.step(1, variant=nat.PROPAGATION_ONLY)
-    s.step(1, variant=nat.READ_WRITE_ONLY)
-    s.macroscopic()
-    s.fields_canonical()
-s = solver.Solver(geo, solver.SimulationConfig(collision="mrt", storage="compact",
-                                               arithmetic="fma"))
-s.step(2)
 solver.GRAPH_STEPS = 4
 s = solver.Solver(geo, solver.SimulationConfig())
 s.step(9, graph=True)
