@@ -38,6 +38,9 @@ namespace step_detail {
 #ifndef TLBM_WARPS_COMPACT_F32
 #define TLBM_WARPS_COMPACT_F32 48
 #endif
+#ifndef TLBM_WARPS_NODES_F32
+#define TLBM_WARPS_NODES_F32 (TLBM_NODES_NPT_F32 == 1 ? 48 : TLBM_NODES_NPT_F32 == 2 ? 32 : 24)
+#endif
 // per (q, j): 64 * (neighbour-row entry of the source tile) + source slot
 struct CompactPull {
     uint16_t w[Q * 64];
@@ -276,14 +279,8 @@ step_kernel_compact(const StepParams<T, MRT> p) {
 #ifndef TLBM_NODES_NPT_F32
 #define TLBM_NODES_NPT_F32 2
 #endif
-// (fp64: two nodes per thread at 16 warps/SM ran 0.853 vs 0.879 at
-// porosity 0.2, scripts/exp/exp51.sh)
 #ifndef TLBM_NODES_NPT_F64
 #define TLBM_NODES_NPT_F64 1
-#endif
-// resident warps per SM of the node-parallel step (sets the register cap)
-#ifndef TLBM_WARPS_NODES_F32
-#define TLBM_WARPS_NODES_F32 (TLBM_NODES_NPT_F32 == 1 ? 48 : TLBM_NODES_NPT_F32 == 2 ? 32 : 24)
 #endif
 #ifndef TLBM_WARPS_NODES_F64
 #define TLBM_WARPS_NODES_F64 (TLBM_NODES_NPT_F64 == 1 ? TLBM_WARPS_COMPACT : 16)

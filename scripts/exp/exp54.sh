@@ -1,0 +1,17 @@
+#!/bin/bash
+# fp64 node-parallel step occupancy: 32 warps/SM (main, 64 registers) vs 36
+# (56 registers, 40 B spill) vs 40 (48 registers, 168 B spill).
+set -u
+O=gpurun_out/exp54
+mkdir -p $O
+for r in 1 2; do
+for lib in main nw36 nw40; do
+  if [ $lib = main ]; then L=""; else L=build/variants/$lib/libtlbm.so; fi
+  TLBM_LIB=$L timeout 600 python scripts/porosity_sweep.py --porosities 0.2,0.5,0.8 --precisions f64 --storages nodes --steps 30 > $O/sweep_${lib}_$r.jsonl 2>$O/sweep_${lib}_$r.err
+done; done
+python - <<'PY'
+import json,glob
+for f in sorted(glob.glob('gpurun_out/exp54/sweep_*.jsonl')):
+    for l in open(f):
+        d=json.loads(l); print(f.split('/')[-1], d['case'], d['precision'], d['storage'], round(d['ms_per_step'],4), round(d['bu'],4))
+PY
