@@ -60,12 +60,14 @@ def periodic_mask(periodic):
 class DeviceTiling:
     """Tile structures of one geometry resident on one GPU.
 
-    types     (nx, ny, nz) uint8        the voxel tags
     tile_map  (ntx, nty, ntz) int32     -1 for empty tiles
     non_empty (t_n, 3) int32            tile corners, scan order
     nbr       (t_n, 27) int32           neighbour tile per delta, -1 absent
     meta      (t_n, 64) uint32          per-slot node word (csrc/d3q19.cuh)
     counts    (t_n,) int32              non-solid nodes per tile
+
+    The voxel tags go to the device only while the tiler runs (1 B/voxel, 2 GB
+    at 2048 x 1024^2); afterwards the step needs only the per-tile arrays.
     """
 
     def __init__(self, geometry, device=None):
@@ -77,12 +79,12 @@ class DeviceTiling:
         nx, ny, nz = self.dims
         self.mesh = tuple(-(-n // TILE) for n in self.dims)
         stream = nat.stream_ptr(self.device)
-        self.types = torch.from_numpy(geometry.types).to(self.device)
+        types = torch.from_numpy(geometry.types).to(self.device)
         self.tile_map = torch.empty(self.mesh, dtype=torch.int32, device=self.device)
         scratch = torch.empty(int(nat.load().tlbm_tiling_scratch_bytes(nx, ny, nz)),
                               dtype=torch.uint8, device=self.device)
         t_n = nat.c_i64(0)
-        nat.call("tlbm_tile_map", nat.ptr(self.types), nx, ny, nz, nat.ptr(self.tile_map),
+        nat.call("tlbm_tile_map", nat.ptr(types), nx, ny, nz, nat.ptr(self.tile_map),
                  nat.ptr(scratch), nat.ctypes.byref(t_n), stream)
         del scratch
         self.t_n = int(t_n.value)
@@ -96,9 +98,10 @@ class DeviceTiling:
                  nat.ptr(self.nbr), stream)
         self.meta = torch.empty((t, 64), dtype=torch.int32, device=self.device)[:self.t_n]
         bad = torch.zeros(2, dtype=torch.int32, device=self.device)
-        nat.call("tlbm_node_meta", nat.ptr(self.types), nx, ny, nz,
+        nat.call("tlbm_node_meta", nat.ptr(types), nx, ny, nz,
                  periodic_mask(self.periodic), nat.ptr(self.non_empty), self.t_n,
                  nat.ptr(self.meta), nat.ptr(bad), stream)
+        del types           # stream-ordered: the caching allocator reuses it after meta
         self.counts = torch.empty(t, dtype=torch.int32, device=self.device)[:self.t_n]
         nat.call("tlbm_tile_counts", nat.ptr(self.meta), self.t_n, nat.ptr(self.counts), stream)
         n_bad_face, n_bad_tag = (int(v) for v in bad.cpu())

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Build an experimental libtlbm.so with extra -D flags on the step kernels:
-#   [ONLY=f32|f64] scripts/build_variant.sh NAME "-DTLBM_MINB=12 -DTLBM_PULL_MODE=2"
+#   [ONLY=f32|f64] [SRC=dir] scripts/build_variant.sh NAME "-DTLBM_MINB=12 -DTLBM_PULL_MODE=2"
 # -> build/variants/NAME/libtlbm.so (select it with TLBM_LIB=...; used by
 # scripts/step_sweep.py tuning runs).  The main objects come from `make`.
 set -eu
@@ -10,7 +10,9 @@ OUT=$ROOT/build/variants/$NAME
 mkdir -p $OUT
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 NV="nvcc -O3 -std=c++20 $ARCH -lineinfo -fmad=false -Xptxas -v -Xcompiler -fPIC -I$ROOT/include --expt-relaxed-constexpr $FLAGS"
-C=$ROOT/paper_1611_02445_b200/csrc
+# SRC=<dir> compiles the step units from a modified copy of csrc/ (an
+# experiment that should not touch the tracked kernel sources)
+C=${SRC:-$ROOT/paper_1611_02445_b200/csrc}
 # ONLY=f32 / ONLY=f64 rebuilds one dtype and links the main build's other one
 O=$ROOT/paper_1611_02445_b200/lib/obj
 for d in f32 f64; do
