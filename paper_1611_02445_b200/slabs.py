@@ -142,7 +142,8 @@ def resolve_auto_storage_global(config, geometry):
 class SlabSolver:
     """One rank's slab: a local Solver plus the halo bookkeeping."""
 
-    def __init__(self, geometry, plan, rank, config=None, device=None, traversal="auto"):
+    def __init__(self, geometry, plan, rank, config=None, device=None, traversal="auto",
+                 initial=(1.0, (0.0, 0.0, 0.0))):
         """``traversal``: "tile" (tile-parallel step), "nodes" (node-parallel
         step over the nodes of each launched tile range; compact storage) or
         "auto" (solver.use_nodes)."""
@@ -162,7 +163,7 @@ class SlabSolver:
             traversal = ("nodes" if use_nodes(config, tiling.n_fn, tiling.t_n, "auto")
                          else "tile")
         self.solver = Solver(self.local_geometry, config, device, tiling=tiling,
-                             traversal=traversal)
+                             traversal=traversal, initial=initial)
         s = self.solver
         layers = layer_tile_ranges(s.tiling.tile_map)
         has_lo, has_hi = self.range.lower >= 0, self.range.upper >= 0
@@ -532,9 +533,9 @@ class DistributedSlabRunner:
     memory instead (tests with several ranks on one GPU)."""
 
     def __init__(self, geometry, world, rank, config=None, device=None, transport="nccl",
-                 traversal="auto"):
+                 traversal="auto", initial=(1.0, (0.0, 0.0, 0.0))):
         self.plan = SlabPlan(geometry, world)
-        self.slab = SlabSolver(geometry, self.plan, rank, config, device, traversal)
+        self.slab = SlabSolver(geometry, self.plan, rank, config, device, traversal, initial)
         self.transport = transport
         self.ipc = None
         self.halo = None

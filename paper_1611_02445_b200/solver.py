@@ -131,7 +131,7 @@ class Solver:
     """Device-resident tiled LBGK solver for one geometry on one GPU."""
 
     def __init__(self, geometry, config=None, device=None, tiling=None, index64=False,
-                 traversal="auto"):
+                 traversal="auto", initial=(1.0, (0.0, 0.0, 0.0))):
         """``index64`` forces the step's 64-bit addressing path (used
         automatically when neighbour offsets exceed 32 bits, i.e. beyond
         ~1.76 M tiles); exposed for tests and measurements.
@@ -149,7 +149,10 @@ class Solver:
         runs the node-parallel step: one thread per non-solid node in store
         order instead of one per tile slot (csrc/step_compact.cuh:
         step_kernel_nodes); "auto" picks it for compact storage below tile
-        utilisation AUTO_NODES_ETA."""
+        utilisation AUTO_NODES_ETA.
+
+        ``initial``: the uniform equilibrium (rho, (ux, uy, uz)) both copies
+        start from (default the cold start rho 1, u 0)."""
         self.config = config if config is not None else SimulationConfig()
         self.geometry = geometry
         self.tiling = tiling if tiling is not None else DeviceTiling(geometry, device)
@@ -216,7 +219,9 @@ class Solver:
         self._graphs = {}
         self._iter_dev = torch.zeros(1, dtype=torch.int64, device=self.device)
         self._iter_dev_value = 0
-        self.init_equilibrium()
+        # the cold start (rho 1, u 0) or the uniform
+        # equilibrium `initial` = (rho, u), written once into both copies
+        self.init_equilibrium(float(initial[0]), tuple(float(v) for v in initial[1]))
 
     # -- initial state -------------------------------------------------------
     def init_equilibrium(self, rho=1.0, u=(0.0, 0.0, 0.0)):
