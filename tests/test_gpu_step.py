@@ -414,14 +414,15 @@ def test_blocked_traversal_bit_identical(storage, dn):
                            torch.arange(s.t_n, device=order.device))
 
 
-@pytest.mark.parametrize("storage", ["blocks", "compact"])
-def test_degenerate_geometries(storage):
+@pytest.mark.parametrize("storage,traversal", [("blocks", "tile"), ("compact", "tile"),
+                                               ("compact", "nodes")])
+def test_degenerate_geometries(storage, traversal):
     """All-solid (no tiles) and single-node geometries step, graph-replay,
-    read out and checkpoint without errors."""
+    read out and checkpoint without errors (both compact kernels)."""
     import tempfile
     cfg = solver.SimulationConfig(u_max_guard=0.0, storage=storage)
     empty = geometry.Geometry(np.zeros((5, 6, 7), np.uint8))
-    s = solver.Solver(empty, cfg)
+    s = solver.Solver(empty, cfg, traversal=traversal)
     assert s.t_n == 0 and s.n_fn == 0
     s.step(3)
     s.step(solver.GRAPH_STEPS, graph=True)
@@ -429,7 +430,8 @@ def test_degenerate_geometries(storage):
     assert rho.shape == (0, 64) and u.shape == (3, 0, 64)
     one = np.zeros((3, 3, 3), np.uint8)
     one[1, 1, 1] = 1                        # a single fluid node, fully enclosed
-    s = solver.Solver(geometry.Geometry(one), cfg)
+    s = solver.Solver(geometry.Geometry(one), cfg, traversal=traversal)
+    assert (s.nodes is not None) == (traversal == "nodes")
     s.step(10)
     rho, _, _ = s.macroscopic()
     assert abs(rho[s.nonsolid_mask()][0] - 1.0) < 1e-15
