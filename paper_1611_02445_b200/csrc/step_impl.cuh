@@ -129,6 +129,15 @@ constexpr int TILE_VALUES = Q * 64;
 
 template <class T>
 constexpr int tiles_per_cta() { return sizeof(T) == 4 ? TLBM_TPC_F32 : TLBM_TPC; }
+// fp64 MRT: one tile per CTA (8 CTAs of 2 warps at 16 warps/SM) staggers the
+// CTAs' gather and product phases: 1.032-1.059 vs 1.062-1.071 ms (reference
+// arithmetic), 0.827-0.830 vs 0.840 (FMA) on the 256^3 channel; LBGK keeps
+// two (scripts/exp/exp60.sh)
+#ifndef TLBM_TPC_MRT
+#define TLBM_TPC_MRT 1
+#endif
+template <class T, bool MRT>
+constexpr int tiles_per_cta_of() { return MRT && sizeof(T) == 8 ? TLBM_TPC_MRT : tiles_per_cta<T>(); }
 
 // (The 64-bit path's earlier formulation -- 64-bit offsets rebuilt per pull --
 // came out of ptxas 12.9 with out-of-bounds addresses at 32 and 40 registers
@@ -144,7 +153,7 @@ constexpr int min_blocks() {
         ? (MRT ? TLBM_WARPS_MRT_F32
                : (VARIANT == TLBM_PROPAGATION_ONLY ? TLBM_WARPS_PROP_F32 : TLBM_WARPS_F32))
         : (MRT ? (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT) : TLBM_WARPS);
-    return warps / (2 * tiles_per_cta<T>());
+    return warps / (2 * tiles_per_cta_of<T, MRT>());
 }
 
 // TLBM_LOAD_MODE (tuning knob): 0 ld.global.nc (default), 1 ld.global,
@@ -414,7 +423,7 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     fill_params<T, MRT, FMA>(p, a);
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
-    constexpr int TPC = tiles_per_cta<T>();
+    constexpr int TPC = tiles_per_cta_of<T, MRT>();
     // the traversal order is a permutation of a whole-store launch; the
     // bench-ladder variants and the halo launches run in tile order
     if constexpr (VARIANT == TLBM_FULL && !HALO) {
