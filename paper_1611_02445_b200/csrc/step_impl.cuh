@@ -114,11 +114,14 @@ constexpr int TILE_VALUES = Q * 64;
 #ifndef TLBM_WARPS_F32
 #define TLBM_WARPS_F32 64
 #endif
-// MRT, reference arithmetic (grouped product, 19 live row sums): 16 warps/SM
-// at 126 registers, 1.054 ms vs 1.083 at 20 (160 B spill) and 1.182 at 24;
-// FMA arithmetic keeps 20 (scripts/exp/exp34.sh)
+// MRT, reference arithmetic (grouped product, 19 live row sums): at one tile
+// per CTA, 20 warps/SM (96 registers, 56 B spill) runs the 256^3 channel in
+// 0.979 ms vs 1.029 at 16 (126 registers) and 1.015 at 24; the compact
+// kernels gain too (node-parallel 0.721 -> 0.757 at porosity 1.0)
+// (scripts/exp/exp62.sh, exp63.sh; at two tiles per CTA 16 had won,
+// exp34.sh).  FMA arithmetic: 24 (0.828 ms vs 0.935 at 28).
 #ifndef TLBM_WARPS_MRT
-#define TLBM_WARPS_MRT 16
+#define TLBM_WARPS_MRT 20
 #endif
 #ifndef TLBM_WARPS_MRT_FMA
 #define TLBM_WARPS_MRT_FMA 24
