@@ -69,7 +69,7 @@ constexpr int compact_tiles_per_cta() { return sizeof(T) == 4 ? 1 : TLBM_TPC_COM
 
 template <class T, bool MRT, int VARIANT, bool FMA = false>
 constexpr int min_blocks_compact() {
-    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32
+    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_COMPACT_MRT_F32
                                   : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
                 : (sizeof(T) == 4 ? TLBM_WARPS_COMPACT_F32 : TLBM_WARPS_COMPACT)) /
            (2 * compact_tiles_per_cta<T>());
@@ -291,7 +291,7 @@ constexpr int nodes_per_thread() {
 }
 template <class T, bool MRT, bool FMA = false>
 constexpr int min_blocks_nodes() {
-    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_MRT_F32
+    return (MRT ? (sizeof(T) == 4 ? TLBM_WARPS_COMPACT_MRT_F32
                                   : (FMA ? TLBM_WARPS_MRT_FMA : TLBM_WARPS_MRT))
                 : (sizeof(T) == 4 ? TLBM_WARPS_NODES_F32 : TLBM_WARPS_NODES_F64)) /
            (TLBM_NODES_THREADS / 32);

@@ -126,8 +126,15 @@ constexpr int TILE_VALUES = Q * 64;
 #ifndef TLBM_WARPS_MRT_FMA
 #define TLBM_WARPS_MRT_FMA 24
 #endif
+// fp32 MRT (packed FMUL2 products): block-store kernel 40 warps/SM (48
+// registers, 68 B spill) 0.624 ms vs 0.636 at 32; the compact kernels keep
+// 32 (node-parallel at 40: 0.544 vs 0.593 of peak at porosity 0.2)
+// (scripts/exp/exp64.sh)
 #ifndef TLBM_WARPS_MRT_F32
-#define TLBM_WARPS_MRT_F32 32
+#define TLBM_WARPS_MRT_F32 40
+#endif
+#ifndef TLBM_WARPS_COMPACT_MRT_F32
+#define TLBM_WARPS_COMPACT_MRT_F32 32
 #endif
 
 template <class T>
