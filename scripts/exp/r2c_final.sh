@@ -5,7 +5,8 @@
 # fp32 MRT), fp32 512^3 tile vs y-blocked DRAM bytes, property test x2000,
 # sanitizers.
 set -u
-O=gpurun_out/r2c_final
+TAG=${1:-r2c_final}
+O=gpurun_out/$TAG
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest_gpu.txt 2>&1
@@ -14,6 +15,9 @@ python bench.py > $O/bench.json 2> $O/bench.err
 python bench.py --impl reference > $O/bench_ref.json 2>> $O/bench.err
 python bench.py --precision f32 --no-cpu --no-sweep > $O/bench_f32.json 2>> $O/bench.err
 python bench.py --arith fma --no-cpu --no-sweep > $O/bench_fma.json 2>> $O/bench.err
+python scripts/step_sweep.py --variants rw,prop,full,mrt --steps 50 > $O/ladder_f64.jsonl 2>/dev/null
+python scripts/step_sweep.py --variants full,mrt --arith fma --steps 50 > $O/ladder_f64_fma.jsonl 2>/dev/null
+python scripts/step_sweep.py --variants rw,prop,full,mrt --precision f32 --steps 50 > $O/ladder_f32.jsonl 2>/dev/null
 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file $O/launches.csv \
     python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --no-sweep > /dev/null 2>&1
 for pr in f64 f32; do
