@@ -12,6 +12,12 @@ step adds except the NVLink transfer latency and the neighbour wait, which
 one GPU cannot show.
 
     python scripts/halo_overhead.py [--ranks 2,4,8] [--precision f64] [--steps 20]
+        [--geometry channel|pack --porosity 0.2 --storage blocks|compact|auto]
+
+``--geometry pack``: the 256^3 sphere pack of BASELINE config 3 cut into N
+slabs (the same domain, so per-slab work shrinks with N), with the storage
+and step that ``--storage`` selects (auto: compact + node-parallel below
+eta_t 0.93).
 """
 import argparse
 import json
@@ -42,20 +48,27 @@ def main():
     p.add_argument("--precision", default="f64")
     p.add_argument("--edge", type=int, default=256)
     p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--geometry", default="channel", choices=["channel", "pack"])
+    p.add_argument("--porosity", type=float, default=0.2)
+    p.add_argument("--storage", default="blocks")
     a = p.parse_args()
-    cfg = SimulationConfig(tau=workloads.TAU, precision=a.precision, u_max_guard=0.0)
+    cfg = SimulationConfig(tau=workloads.TAU, precision=a.precision, u_max_guard=0.0,
+                           storage=a.storage)
+    pack = workloads.sphere_pack(a.porosity, n=a.edge) if a.geometry == "pack" else None
     for n in (int(v) for v in a.ranks.split(",")):
-        geo = workloads.channel_z(a.edge, a.edge * n)
+        geo = pack if pack is not None else workloads.channel_z(a.edge, a.edge * n)
         s = Solver(geo, cfg)
         s.init_equilibrium(1.0, (0.0, 0.0, 0.04))
         t_one = timed(lambda k: s.step(k, check=False), a.steps)
         n_fn = s.n_fn
         del s
         torch.cuda.empty_cache()
-        rec = {"ranks": n, "precision": a.precision, "dims": list(geo.shape), "n_fn": n_fn,
+        rec = {"ranks": n, "precision": a.precision, "geometry": a.geometry,
+               "storage": a.storage, "dims": list(geo.shape), "n_fn": n_fn,
                "ms_one_domain": t_one}
         for fused in (True, False):
             vs = slabs.VirtualSlabs(geo, n, cfg, fused=fused)
+            rec["nodes_step"] = all(sl.solver.nodes is not None for sl in vs.slabs)
             for sl in vs.slabs:
                 sl.solver.init_equilibrium(1.0, (0.0, 0.0, 0.04))
             t = timed(vs.step, a.steps)
