@@ -350,8 +350,16 @@ __device__ __forceinline__ uint32_t mrt_deviations(const T (&g)[Q], T (&d)[Q], T
 // distinct values of a column; the row sums stay scalar FADDs, which ptxas
 // does not contract with a packed product.  Columns start at even offsets
 // of the operator table (mrt_offset_even) so each pair is one 8-byte load.
+// 0: scalar, 1: packed products (FMUL2), 2: packed products and row sums
+// (FFMA2 + FADD2, below).  The block-store kernel runs 2 (256^3 channel
+// 0.623 -> 0.586 ms at 32 warps/SM); the compact kernels run 1 (the
+// node-parallel step holds two nodes per thread and loses with 2:
+// porosity 0.2 0.1345 -> 0.141 ms) (scripts/exp/exp71.sh)
 #ifndef TLBM_MRT_PACKED
-#define TLBM_MRT_PACKED 1
+#define TLBM_MRT_PACKED 2
+#endif
+#ifndef TLBM_MRT_PACKED_COMPACT
+#define TLBM_MRT_PACKED_COMPACT 1
 #endif
 __host__ __device__ constexpr int mrt_offset_even(int j) {
     int o = 0;
@@ -359,9 +367,9 @@ __host__ __device__ constexpr int mrt_offset_even(int j) {
     return o;
 }
 // where column j's distinct values start in the kernel's operator table
-template <class T>
+template <class T, int PACK>
 __host__ __device__ constexpr int mrt_table_offset(int j) {
-    return (sizeof(T) == 4 && TLBM_MRT_PACKED) ? mrt_offset_even(j) : mrt_offset(j);
+    return (sizeof(T) == 4 && PACK == 1) ? mrt_offset_even(j) : mrt_offset(j);
 }
 __device__ __forceinline__ void mul2_bcast(const float *c, float d, float &r0, float &r1) {
     unsigned long long cc, dd, rr;
@@ -371,18 +379,89 @@ __device__ __forceinline__ void mul2_bcast(const float *c, float d, float &r0, f
     asm("mov.b64 {%0, %1}, %2;" : "=f"(r0), "=f"(r1) : "l"(rr));
 }
 
-template <class T, int QUASI>
+// TLBM_MRT_PACKED 2: the row sums too, two rows per FADD2 (add.rn.f32x2,
+// bit-identical to two FADDs).  Rows are paired (mrt_pair_row); for each
+// column the pairs' product pairs (c_a d, c_b d) come from one packed
+// multiply per distinct (value, value) combination (mrt_combo_group).  The
+// multiply is fma.rn.f32x2(c, d, -0): c*d + (-0) rounds the exact product
+// once, so it equals mul.rn bit for bit (an exact +0 product stays +0), and
+// ptxas cannot contract it into the following FADD2 -- it does contract
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2 even under -fmad=false.  The -0
+// pair is loaded from global memory (tlbm_neg_zero2), opaque to ptxas and in
+// an ordinary register, so every coefficient pair stays a uniform-register
+// operand (LDCU.128, two pairs per load); from the kernel parameters it
+// would be uniform too and push the coefficients into LDC.64 + registers.
+static __device__ unsigned long long tlbm_neg_zero2 = 0x8000000080000000ull;
+__device__ __forceinline__ unsigned long long fma2_bcast_zero(const float *c, float d,
+                                                              unsigned long long z) {
+    unsigned long long cc, dd, rr;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "f"(c[0]), "f"(c[1]));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(dd) : "f"(d));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rr) : "l"(cc), "l"(dd), "l"(z));
+    return rr;
+}
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float lane_of(unsigned long long v, int h) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    return h ? hi : lo;
+}
+
+__device__ __forceinline__ void mrt_product_paired(float (&g)[Q], const float (&d)[Q],
+                                                   const float *op) {
+    const unsigned long long z = tlbm_neg_zero2;
+    unsigned long long acc[kMrtPairs];
+    float acc_s = 0.f;
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        unsigned long long pr[kMrtMaxCombos];
+#pragma unroll
+        for (int c = 0; c < kMrtMaxCombos; ++c)
+            if (c < mrt_ncombo(j))
+                pr[c] = fma2_bcast_zero(op + 2 * (mrt_combo_offset(j) + c), d[j], z);
+#pragma unroll
+        for (int p = 0; p < kMrtPairs; ++p)
+            acc[p] = j == 0 ? pr[mrt_pair_combo(p, j)] : add2(acc[p], pr[mrt_pair_combo(p, j)]);
+        constexpr int kNone = -1;
+        const float ps = mrt_single_lane(j) != kNone
+                             ? lane_of(pr[mrt_single_lane(j) >> 1], mrt_single_lane(j) & 1)
+                             : op[mrt_single_offset(j)] * d[j];
+        acc_s = j == 0 ? ps : acc_s + ps;
+    }
+#pragma unroll
+    for (int p = 0; p < kMrtPairs; ++p) {
+        g[mrt_pair_row(p, 0)] = g[mrt_pair_row(p, 0)] + lane_of(acc[p], 0);
+        g[mrt_pair_row(p, 1)] = g[mrt_pair_row(p, 1)] + lane_of(acc[p], 1);
+    }
+    g[kMrtSingleRow] = g[kMrtSingleRow] + acc_s;
+}
+
+// PACK: the fp32 packing (TLBM_MRT_PACKED); the operator table's layout
+// follows it (fill_params)
+template <class T, int QUASI, int PACK = 0>
 __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq,
                                                 bool grouped = false) {
     T d[Q];
     const uint32_t st = mrt_deviations<T, QUASI>(g, d, guard_sq);
+    if constexpr (sizeof(T) == 4 && PACK == 2) {
+        if (TLBM_MRT_GROUPED && grouped) {
+            mrt_product_paired(reinterpret_cast<float (&)[Q]>(g),
+                               reinterpret_cast<const float (&)[Q]>(d),
+                               reinterpret_cast<const float *>(op));
+            return st;
+        }
+    }
     if (TLBM_MRT_GROUPED && grouped) {
         T acc[Q];
 #pragma unroll
         for (int j = 0; j < Q; ++j) {
             T prod[kMrtMaxPerColumn];
-            constexpr bool kPacked = sizeof(T) == 4 && TLBM_MRT_PACKED;
-            const int o = mrt_table_offset<T>(j);
+            constexpr bool kPacked = sizeof(T) == 4 && PACK == 1;
+            const int o = mrt_table_offset<T, PACK>(j);
 #pragma unroll
             for (int k = 0; k < kMrtMaxPerColumn; ++k) {
                 if (k >= mrt_count(j)) continue;

@@ -103,7 +103,8 @@ __device__ __forceinline__ uint32_t compact_finish(const StepParams<T, MRT> &p, 
             if constexpr (MRT && FMA)
                 status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
             else if constexpr (MRT)
-                status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
+                status = collide_mrt<T, QUASI, TLBM_MRT_PACKED_COMPACT>(g, p.mrt.op, T(p.guard_sq),
+                                                                        p.mrt.grouped);
             else if constexpr (FMA)
                 status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
             else

@@ -126,12 +126,13 @@ constexpr int TILE_VALUES = Q * 64;
 #ifndef TLBM_WARPS_MRT_FMA
 #define TLBM_WARPS_MRT_FMA 24
 #endif
-// fp32 MRT (packed FMUL2 products): block-store kernel 40 warps/SM (48
-// registers, 68 B spill) 0.624 ms vs 0.636 at 32; the compact kernels keep
-// 32 (node-parallel at 40: 0.544 vs 0.593 of peak at porosity 0.2)
-// (scripts/exp/exp64.sh)
+// fp32 MRT: the block-store kernel (packed row sums, TLBM_MRT_PACKED 2) at
+// 32 warps/SM (no spill) 0.586 ms vs 0.623 at 40; with packed products only
+// 40 had won (0.624 vs 0.636 at 32); the compact kernels keep 32
+// (node-parallel at 40: 0.544 vs 0.593 of peak at porosity 0.2)
+// (scripts/exp/exp64.sh, exp71.sh)
 #ifndef TLBM_WARPS_MRT_F32
-#define TLBM_WARPS_MRT_F32 40
+#define TLBM_WARPS_MRT_F32 32
 #endif
 #ifndef TLBM_WARPS_COMPACT_MRT_F32
 #define TLBM_WARPS_COMPACT_MRT_F32 32
@@ -326,7 +327,8 @@ step_kernel(const StepParams<T, MRT> p) {
                 if constexpr (MRT && FMA)
                     status = collide_mrt_fma<T, QUASI>(g, p.mrt.op, T(p.guard_sq));
                 else if constexpr (MRT)
-                    status = collide_mrt<T, QUASI>(g, p.mrt.op, T(p.guard_sq), p.mrt.grouped);
+                    status = collide_mrt<T, QUASI, TLBM_MRT_PACKED>(g, p.mrt.op, T(p.guard_sq),
+                                                                    p.mrt.grouped);
                 else if constexpr (FMA)
                     status = collide_fma<T, QUASI>(g, T(p.inv_tau), T(p.guard_sq));
                 else
@@ -424,13 +426,13 @@ int launch(const tlbm_step_args *a, cudaStream_t s) {
     return launch_arith<T, QUASI, TABLE, VARIANT, false, false>(a, s);
 }
 
-template <class T, bool MRT, bool FMA>
+template <class T, bool MRT, bool FMA, int PACK>
 void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a);
 
 template <class T, int QUASI, int TABLE, int VARIANT, bool REL32, bool MRT, bool HALO, bool FMA>
 int launch_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
-    fill_params<T, MRT, FMA>(p, a);
+    fill_params<T, MRT, FMA, TLBM_MRT_PACKED>(p, a);
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int TPC = tiles_per_cta_of<T, MRT>();
@@ -451,7 +453,7 @@ int launch_as(const tlbm_step_args *a, cudaStream_t s) {
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA>
 int launch_nodes(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
-    fill_params<T, MRT, FMA>(p, a);
+    fill_params<T, MRT, FMA, TLBM_MRT_PACKED_COMPACT>(p, a);
     const long long n = a->node_end - a->node_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int per_cta = TLBM_NODES_THREADS * nodes_per_thread<T, MRT>();
@@ -468,7 +470,7 @@ int launch_nodes(const tlbm_step_args *a, cudaStream_t s) {
 template <class T, int QUASI, int TABLE, int VARIANT, bool MRT, bool FMA>
 int launch_compact_as(const tlbm_step_args *a, cudaStream_t s) {
     StepParams<T, MRT> p;
-    fill_params<T, MRT, FMA>(p, a);
+    fill_params<T, MRT, FMA, TLBM_MRT_PACKED_COMPACT>(p, a);
     const long long n = a->tile_end - a->tile_begin;
     if (n <= 0) return TLBM_OK;
     constexpr int TPC = compact_tiles_per_cta<T>();
@@ -576,7 +578,7 @@ inline bool mrt_moment_rates(const double *A, double *w) {
     return last_ok;
 }
 
-template <class T, bool MRT, bool FMA>
+template <class T, bool MRT, bool FMA, int PACK>
 void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
     if constexpr (MRT) {
         // op.astype(dtype); grouped when every column's equal-value rows of
@@ -595,10 +597,20 @@ void fill_params(StepParams<T, MRT> &p, const tlbm_step_args *a) {
         p.mrt.grouped = grouped;
         if (FMA)
             for (int k = 0; k < Q; ++k) p.mrt.op[k] = T(w[k]);
-        else if (grouped)
+        else if (grouped && sizeof(T) == 4 && PACK == 2) {
+            // (c_a, c_b) per combination, then the single row's scalars
+            auto val = [&](int j, int k) { return T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]); };
+            for (int j = 0; j < Q; ++j) {
+                for (int c = 0; c < mrt_ncombo(j); ++c)
+                    for (int h = 0; h < 2; ++h)
+                        p.mrt.op[2 * (mrt_combo_offset(j) + c) + h] = val(j, mrt_combo_group(j, c, h));
+                if (mrt_single_offset(j) >= 0)
+                    p.mrt.op[mrt_single_offset(j)] = val(j, mrt_group(kMrtSingleRow, j));
+            }
+        } else if (grouped)
             for (int j = 0; j < Q; ++j)
                 for (int k = 0; k < mrt_count(j); ++k)
-                    p.mrt.op[mrt_table_offset<T>(j) + k] =
+                    p.mrt.op[mrt_table_offset<T, PACK>(j) + k] =
                         T(a->mrt_op[mrt_rep(mrt_offset(j) + k) * Q + j]);
         else
             for (int k = 0; k < Q * Q; ++k) p.mrt.op[k] = T(a->mrt_op[k]);

@@ -171,11 +171,23 @@ def test_mrt_pattern_header_is_current():
     assert open(gen.OUT).read() == gen.render()
     from paper_1611_02445_b200 import collision
     txt = gen.render()
+    grp = txt[txt.index("mrt_group(int i, int j)"):txt.index("mrt_rep(int n)")]
     pat = np.array([[int(v) for v in r.split(",")]
-                    for r in re.findall(r"\{([0-9, ]+)\},", txt)])
+                    for r in re.findall(r"\{([0-9, ]+)\},", grp)])
     assert pat.shape == (19, 19)
     for tau in (0.6, 0.9, 1.7):
         op = collision.mrt_operator(collision.default_mrt_rates(tau))
         for j in range(19):
             for g in set(pat[:, j]):
                 assert len({op[i, j].tobytes() for i in np.flatnonzero(pat[:, j] == g)}) == 1
+    # the fp32 packed row sums: every row pair's product pair in every column
+    # is one of the column's combinations, lane for lane
+    combos, which, lane = gen.pairs_cost(pat)
+    assert sum(len(c) for c in combos) == 129
+    rows = sorted(sum(map(list, gen.ROW_PAIRS), [gen.SINGLE_ROW]))
+    assert rows == list(range(19))
+    for j in range(19):
+        for p, (i, k) in enumerate(gen.ROW_PAIRS):
+            assert combos[j][which[j][p]] == (pat[i, j], pat[k, j])
+        if lane[j] >= 0:
+            assert combos[j][lane[j] >> 1][lane[j] & 1] == pat[gen.SINGLE_ROW, j]
