@@ -15,8 +15,8 @@ cp $O/bench_fma.json $D/${P}_bench_n1_fma.json
 cp $O/smoke.txt $D/${P}_smoke.txt
 tail -15 $O/pytest_gpu.txt > $D/${P}_pytest_gpu_summary.txt
 cp $O/property_2000.txt $D/${P}_property_2000.txt
-cp $O/memcheck.txt $D/${P}_memcheck.txt
-cp $O/racecheck.txt $D/${P}_racecheck.txt
+[ -f $O/memcheck.txt ] && cp $O/memcheck.txt $D/${P}_memcheck.txt
+[ -f $O/racecheck.txt ] && cp $O/racecheck.txt $D/${P}_racecheck.txt
 cp $O/launches.csv $D/${P}_launches_channel256_f64.csv
 cat $O/ladder_*.jsonl 2>/dev/null | grep '^{' > $D/${P}_ladder.jsonl || true
 for pr in f64 f32; do

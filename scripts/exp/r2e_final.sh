@@ -2,8 +2,8 @@
 # Round-2 final evidence pass (run on the final code): smoke, pytest -m gpu,
 # bench lines (default, reference arm, fp32, fma), ncu launch list and full
 # captures (bench step f64/f32 -> roofline traffic; node-parallel p0.2;
-# fp32 MRT), fp32 512^3 tile vs y-blocked DRAM bytes, property test x2000,
-# sanitizers.
+# fp32 MRT), fp32 512^3 tile vs y-blocked DRAM bytes, property test x2000
+# (compute-sanitizer is closed on this pool; r2c/r2d ran it).
 set -u
 TAG=${1:-r2e_final}
 O=gpurun_out/$TAG
@@ -44,8 +44,5 @@ for tr in tile auto; do
 done
 TLBM_PROPERTY_EXAMPLES=2000 timeout 2400 python -m pytest tests/test_gpu_property.py -m gpu -q --hypothesis-show-statistics > $O/property_2000.txt 2>&1
 tail -3 $O/property_2000.txt
-timeout 900 compute-sanitizer --tool memcheck python scripts/sanitize_small.py > $O/memcheck.txt 2>&1
-timeout 900 compute-sanitizer --tool racecheck python scripts/sanitize_small.py > $O/racecheck.txt 2>&1
-tail -2 $O/memcheck.txt $O/racecheck.txt
 du -sh $O
 ls -la $O/*.ncu-rep
