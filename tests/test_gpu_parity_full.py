@@ -181,6 +181,22 @@ def test_step_sphere_pack_256_p05_quasi_mrt(c_oracle):
     _step_parity(c_oracle, s, geo)
 
 
+@pytest.mark.parametrize("geometry,storage", [("channel", "blocks"), ("pack02", "compact")])
+def test_step_mrt_f32_full_size(c_oracle, geometry, storage):
+    """fp32 MRT at BASELINE size, bit-exact vs the C oracle over 10 steps:
+    the 256^3 channel on the block store (packed products and packed row
+    sums, FFMA2(c, d, -0) + FADD2) and the porosity-0.2 pack on the compact
+    store (node-parallel step, packed products only)."""
+    geo = workloads.channel_z(256) if geometry == "channel" else workloads.sphere_pack(0.2)
+    cfg = SimulationConfig(collision="mrt", tau=workloads.TAU, precision="f32",
+                           storage=storage)
+    s = Solver(geo, cfg)
+    assert (s.nodes is not None) == (storage == "compact")
+    rho, u = workloads.perturbed_fields(s.t_n, s.store.tdtype, s.device, (0.0, 0.0, 0.02))
+    s.init_from_macroscopic(rho, u)
+    _step_parity(c_oracle, s, geo)
+
+
 @pytest.mark.parametrize("storage", ["blocks", "auto"])
 def test_step_vessel_tree_256x256x512(c_oracle, storage):
     """BASELINE config 4 at half edge: velocity inlet z = 0, pressure outlet
