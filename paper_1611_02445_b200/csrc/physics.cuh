@@ -299,34 +299,44 @@ __device__ __forceinline__ uint32_t collide(T (&g)[Q], T inv_tau, T guard_sq) {
     return status_of<T, QUASI>(rho, usq, guard_sq);
 }
 
-// feq - g in the reference's order (collision.py:94-121, 244-246): the
-// deviations the MRT operator is applied to; returns the status word
+// feq - g in the reference's order (collision.py:94-121, 244-246) for
+// direction q and, with it, opp(q) (they share c.u, 3 cu and 4.5 cu cu):
+// the deviations the MRT operator is applied to.  q with opp(q) < q is
+// done by its partner.
+template <class T, int QUASI>
+__device__ __forceinline__ void mrt_dev_at(int q, const T (&g)[Q], T (&d)[Q], T rho,
+                                           const T (&u)[3], T c15) {
+    if (q == 0) {
+        d[0] = feq_of<T, QUASI>(0, rho, (T(3.0) * T(0) + T(4.5) * T(0) * T(0)) - c15) - g[0];
+        return;
+    }
+    if (opp(q) < q) return;
+    const int o = opp(q);
+    T cu = T(0);
+    bool first = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const int e = e_axis(q, a);
+        if (e == 0) continue;
+        const T term = e > 0 ? u[a] : -u[a];
+        cu = first ? term : cu + term;
+        first = false;
+    }
+    const T A = T(3.0) * cu;
+    const T B = T(4.5) * cu * cu;
+    d[q] = feq_of<T, QUASI>(q, rho, (A + B) - c15) - g[q];
+    d[o] = feq_of<T, QUASI>(o, rho, (B - A) - c15) - g[o];
+}
+
+// all 19 deviations; returns the status word
 template <class T, int QUASI>
 __device__ __forceinline__ uint32_t mrt_deviations(const T (&g)[Q], T (&d)[Q], T guard_sq) {
     T rho, u[3];
     moments<T, QUASI>(g, rho, u);
     const T usq = speed_sq(u);
     const T c15 = T(1.5) * usq;
-    d[0] = feq_of<T, QUASI>(0, rho, (T(3.0) * T(0) + T(4.5) * T(0) * T(0)) - c15) - g[0];
 #pragma unroll
-    for (int q = 1; q < Q; ++q) {
-        if (opp(q) < q) continue;
-        const int o = opp(q);
-        T cu = T(0);
-        bool first = true;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int e = e_axis(q, a);
-            if (e == 0) continue;
-            const T term = e > 0 ? u[a] : -u[a];
-            cu = first ? term : cu + term;
-            first = false;
-        }
-        const T A = T(3.0) * cu;
-        const T B = T(4.5) * cu * cu;
-        d[q] = feq_of<T, QUASI>(q, rho, (A + B) - c15) - g[q];
-        d[o] = feq_of<T, QUASI>(o, rho, (B - A) - c15) - g[o];
-    }
+    for (int q = 0; q < Q; ++q) mrt_dev_at<T, QUASI>(q, g, d, rho, u, c15);
     return status_of<T, QUASI>(rho, usq, guard_sq);
 }
 
@@ -445,16 +455,31 @@ __device__ __forceinline__ void mrt_product_paired(float (&g)[Q], const float (&
 template <class T, int QUASI, int PACK = 0>
 __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_sq,
                                                 bool grouped = false) {
-    T d[Q];
-    const uint32_t st = mrt_deviations<T, QUASI>(g, d, guard_sq);
+    // (computing each column's deviations right before its products instead
+    // of all 19 up front frees registers but ran 1.7% / 1.0% slower in
+    // fp64 / fp32 on the 256^3 channel, scripts/exp/exp74.sh)
     if constexpr (sizeof(T) == 4 && PACK == 2) {
         if (TLBM_MRT_GROUPED && grouped) {
+            // the status word before the deviations -- the same operations,
+            // scheduled by ptxas into 0.568 vs 0.586 ms on the 256^3
+            // channel (fp64's grouped product the other way round: 1.010 vs
+            // 0.986 ms; scripts/exp/exp75.sh)
+            T rho, u[3];
+            moments<T, QUASI>(g, rho, u);
+            const T usq = speed_sq(u);
+            const T c15 = T(1.5) * usq;
+            const uint32_t st = status_of<T, QUASI>(rho, usq, guard_sq);
+            T d[Q];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) mrt_dev_at<T, QUASI>(q, g, d, rho, u, c15);
             mrt_product_paired(reinterpret_cast<float (&)[Q]>(g),
                                reinterpret_cast<const float (&)[Q]>(d),
                                reinterpret_cast<const float *>(op));
             return st;
         }
     }
+    T d[Q];
+    const uint32_t st = mrt_deviations<T, QUASI>(g, d, guard_sq);
     if (TLBM_MRT_GROUPED && grouped) {
         T acc[Q];
 #pragma unroll
@@ -482,14 +507,14 @@ __device__ __forceinline__ uint32_t collide_mrt(T (&g)[Q], const T *op, T guard_
         }
 #pragma unroll
         for (int i = 0; i < Q; ++i) g[i] = g[i] + acc[i];
-    } else {
+        return st;
+    }
 #pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            T acc = T(0);
+    for (int i = 0; i < Q; ++i) {
+        T acc = T(0);
 #pragma unroll
-            for (int j = 0; j < Q; ++j) acc = acc + op[i * Q + j] * d[j];
-            g[i] = g[i] + acc;
-        }
+        for (int j = 0; j < Q; ++j) acc = acc + op[i * Q + j] * d[j];
+        g[i] = g[i] + acc;
     }
     return st;
 }
